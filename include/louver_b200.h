@@ -1,0 +1,199 @@
+/*
+ * louver_b200.h — C ABI of the B200-native Louver decode hot path.
+ *
+ * One lv_ctx holds ONE attention layer's KV cache for `batch` independent
+ * sequences x `n_kv_heads` KV heads (a "slot" = one (sequence, kv head)
+ * pair), the device index over it (contiguous cells with AABB summaries), and
+ * the scratch its queries need. Grouped-query attention: q head hq reads kv
+ * head hq / group_size (Llama convention).
+ *
+ * The entry points replace the reference library API (paths relative to
+ * /root/reference/proj):
+ *   lv_create / lv_destroy  — LouverCache(int, BuildConfig, size_t)        include/louver/cache.hpp:24-29
+ *   lv_build                — LouverCache(KeyStore, BuildConfig, size_t) +  include/louver/cache.hpp:31-36
+ *                             build_index(const KeyStore&, const BuildConfig&) include/louver/index.hpp:79
+ *   lv_push_key             — LouverCache::push_key                        include/louver/cache.hpp:38, src/cache.cpp:7-10
+ *   lv_flush                — LouverCache::flush_buffer                    include/louver/cache.hpp:41, src/cache.cpp:12-22
+ *   lv_query                — LouverCache::query (filter + exact_check +   include/louver/cache.hpp:46-47, src/cache.cpp:30-70
+ *                             dense buffer scan + sparse_attention)
+ *   lv_brute_force_range    — brute_force_range                            include/louver/query.hpp:44-45, src/query.cpp:11-20
+ *   lv_sparse_attention     — sparse_attention                              include/louver/query.hpp:69-72, src/query.cpp:338-371
+ *   lv_dense_decode         — (no reference counterpart) full-scan decode, the speed-up denominator
+ *   lv_lse_merge            — (no reference counterpart) log-sum-exp merge of sequence-sharded partials
+ *
+ * Status codes map onto the reference's error behaviour: LV_EINVAL <-
+ * std::invalid_argument, LV_ERANGE <- std::out_of_range, LV_ERUNTIME <-
+ * std::runtime_error, LV_EMPTY <- std::nullopt / `false` (empty attention set,
+ * empty flush). lv_last_error() returns the message of the calling thread's
+ * last failure.
+ *
+ * Memory: pointers tagged `where` are host (LV_HOST; copies happen inside the
+ * call on `stream`, which is then synchronised) or device (LV_DEVICE; the call
+ * only enqueues work on `stream`). `stream` is a cudaStream_t (NULL = legacy
+ * default stream).
+ *
+ * Threading (cache.hpp:18-20): single writer — lv_build / lv_push_key /
+ * lv_flush need exclusive access; lv_query is re-entrant across threads and
+ * streams when each caller passes its own `workspace` (see
+ * lv_query_workspace_bytes); with workspace == NULL the context's internal
+ * workspace is used and concurrent queries on one context must be serialised.
+ */
+#ifndef LOUVER_B200_H
+#define LOUVER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LV_OK 0
+#define LV_EMPTY 1
+#define LV_EINVAL (-1)
+#define LV_ERANGE (-2)
+#define LV_ERUNTIME (-3)
+#define LV_ENODEV (-4)
+
+#define LV_F32 0
+#define LV_BF16 1
+
+#define LV_HOST 0
+#define LV_DEVICE 1
+
+/* FilterAlgo (cache.hpp:7). Both select the same final set; on the device
+ * both run the fused cell probe (the per-cell AABB bound summed over all
+ * coordinates is at least as strong as either reference filter). */
+#define LV_ALGO_FULL_SUBSPACE 0
+#define LV_ALGO_TA 1
+
+typedef struct lv_ctx lv_ctx;
+
+typedef struct {
+    int d;                   /* head dimension, 1..256 */
+    int n_kv_heads;          /* H_kv >= 1 */
+    int group_size;          /* G = H_q / H_kv, one of 1, 2, 4, 8 */
+    int batch;               /* independent sequences >= 1 */
+    int dtype;               /* K/V storage: LV_F32 or LV_BF16 (summaries use the same type) */
+    /* BuildConfig (index.hpp:10-22). The device index groups keys into
+     * contiguous cells of `r` keys (r rounded up to a power of two, <= 64) with
+     * one AABB per cell; S, grouping, enclosure and rng_seed are validated like
+     * the reference and recorded, but only change pruning statistics — the
+     * selected set and the attention output do not depend on them (SURVEY
+     * Executive summary item 3). */
+    int S;
+    int r;
+    int grouping;            /* 0 contiguous, 1 interleaved, 2 random, 3 pca_tree */
+    int enclosure;           /* 0 ball, 1 aabb, 2 span_ball */
+    uint64_t rng_seed;
+    int64_t buffer_capacity; /* B >= 1: keys [indexed_count, n) form the dense-scanned buffer */
+    int64_t capacity;        /* max keys per sequence held in the HBM arena */
+} lv_config;
+
+typedef struct {
+    const float* q;     /* [batch][H_q][d] fp32 */
+    const float* tau;   /* [batch][H_q] fp32, applied to the unscaled normative q.k */
+    float scale;        /* softmax scale; 0 -> 1/sqrt(d) (query.hpp:17-19) */
+    int algo;           /* LV_ALGO_*; accepted for API parity */
+    int strict;         /* 0: attend selected ∪ buffer (default); 1: attend selected only */
+    int where;          /* LV_HOST or LV_DEVICE for q, tau, out, partial, counts */
+    float* out;         /* [batch][H_q][d] attention output; rows with an empty set are 0 */
+    float* partial;     /* optional [batch][H_q][d+2]: (m, l, o[d]) with o unnormalised,
+                           for lv_lse_merge across sequence shards */
+    int32_t* counts;    /* optional [batch][H_q][4]: selected, attended, keys_scanned, has_attn */
+    uint32_t* sel_bits; /* optional DEVICE [batch][H_q][lv_bitmap_words()] bitmap of selected ids */
+    uint64_t* totals;   /* optional DEVICE [4]: cells probed, cells surviving (union over the
+                           group), keys loaded (union), values loaded (union) — summed over slots */
+    void* workspace;    /* optional DEVICE scratch of lv_query_workspace_bytes() bytes */
+    void* stream;       /* cudaStream_t */
+} lv_query_args;
+
+const char* lv_last_error(void);
+
+/* Version string and the device the library was compiled for ("sm_100a"). */
+const char* lv_build_info(void);
+
+int lv_create(const lv_config* cfg, lv_ctx** out);
+int lv_destroy(lv_ctx* ctx);
+
+/* Prefill: adopt n keys/values per slot and index them all (the adopting
+ * constructor, cache.hpp:31-36). K, V: [batch][H_kv][n][d] of `src_dtype`
+ * (LV_F32 always accepted; LV_BF16 when the storage dtype is bf16). Replaces
+ * any previous contents. n == 0 leaves an empty cache. */
+int lv_build(lv_ctx* ctx, const void* K, const void* V, int64_t n, int src_dtype, int where,
+             void* stream);
+
+/* Grow the arena to hold `capacity` keys per sequence, keeping every stored
+ * row, summary and counter (KeyStore's geometric regrowth, core.hpp:156-162).
+ * Invalidates caller workspaces sized by lv_query_workspace_bytes(). */
+int lv_reserve(lv_ctx* ctx, int64_t capacity, void* stream);
+
+/* Append one key/value per slot (k, v: [batch][H_kv][d] of src_dtype) and fold
+ * it into the open cell's summary in place; when pending >= B the buffer is
+ * flushed (cache.cpp:7-10). Enqueue-only for LV_DEVICE: the counters live on
+ * the device, so the call is CUDA-graph capturable. */
+int lv_push_key(lv_ctx* ctx, const void* k, const void* v, int src_dtype, int where,
+                void* stream);
+
+/* cache.cpp:12-22: returns LV_EMPTY (no-op) when nothing is pending. */
+int lv_flush(lv_ctx* ctx, void* stream);
+
+int lv_query(lv_ctx* ctx, const lv_query_args* args);
+size_t lv_query_workspace_bytes(const lv_ctx* ctx);
+int64_t lv_bitmap_words(const lv_ctx* ctx);
+
+/* Host mirrors of the device counters (uniform over slots). */
+int64_t lv_n(const lv_ctx* ctx);
+int64_t lv_indexed_count(const lv_ctx* ctx);
+int64_t lv_pending_count(const lv_ctx* ctx);
+int64_t lv_flush_count(const lv_ctx* ctx);
+
+/* Refresh the host mirrors from the device counters (needed after replaying a
+ * captured CUDA graph that contains lv_push_key). */
+int lv_sync_counters(lv_ctx* ctx, void* stream);
+
+/* Read back stored keys/values of one slot as fp32 rows [count][d] (host). */
+int lv_read_rows(const lv_ctx* ctx, int slot, int64_t first, int64_t count, int which_v,
+                 float* out);
+
+/* query.cpp:11-20 on the device: bitmap of ids j < limit with dot(q, k_j) >= tau
+ * for every q head (normative dot, bit-exact). q, tau as in lv_query (`where`
+ * applies to them); sel_bits is DEVICE [batch][H_q][lv_bitmap_words()]. */
+int lv_brute_force_range(lv_ctx* ctx, const float* q, const float* tau, int64_t limit, int where,
+                         uint32_t* sel_bits, void* stream);
+
+/* Expand bitmaps to ascending id lists on the device: ids[row][..] gets the set
+ * bits of row `row` below `limit`; count[row] the number written. */
+int lv_bitmap_to_ids(const uint32_t* bits, int64_t words, int64_t rows, int64_t limit,
+                     uint32_t* ids, int64_t ids_stride, int32_t* count, void* stream);
+
+/* query.cpp:338-371 for ONE q head: tokens = sort∪unique(selected ∪ buffer)
+ * (ids of slot `slot`), scores = scale·normative dot, softmax, output. ids are
+ * host or device per `where`; out[d] and optional weights[ntok] likewise.
+ * Returns LV_EMPTY when the token set is empty. */
+int lv_sparse_attention(lv_ctx* ctx, int slot, const uint32_t* buffer_ids, int64_t nbuf,
+                        const uint32_t* selected_ids, int64_t nsel, const float* q, float scale,
+                        int where, float* out, float* weights, int64_t* ntok, void* stream);
+
+/* Full-scan decode over keys [0, n) of every slot (fused split-K online
+ * softmax, GQA-grouped). Same q/out conventions as lv_query. */
+int lv_dense_decode(lv_ctx* ctx, const float* q, float scale, int where, float* out,
+                    float* partial, void* stream);
+
+/* Log-sum-exp merge of P shard partials [P][rows][d+2] (m, l, o unnormalised)
+ * into out[rows][d] (device pointers). Empty shards carry m = -inf, l = 0. */
+int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream);
+
+/* Host-side synthetic streams with the reference laws (io.cpp:89-206);
+ * exported by liblouver_synth.so. */
+int lv_synth_keys(int64_t n, int d, uint64_t seed, float* out);
+int lv_synth_queries(int64_t nq, int d, uint64_t seed, float* out);
+int lv_synth_mixture(int64_t n, int d, int k, double spread, uint64_t seed, int queries,
+                     float* out);
+int lv_synth_keys_multi(int64_t n, int d, const uint64_t* seeds, int64_t nstreams, float* out,
+                        int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

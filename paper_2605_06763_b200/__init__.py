@@ -1,0 +1,26 @@
+"""B200-native Louver decode hot path (arxiv 2605.06763).
+
+For each decode query: retrieve every cached key with q·k >= tau (zero false
+negatives, bit-exact against the reference's normative fp32 dot) and attend
+over exactly that set, on sm_100a kernels behind the C ABI in
+include/louver_b200.h. See DESIGN.md.
+"""
+from ._capi import LouverError, LIB_PATH, SYNTH_PATH  # noqa: F401
+from .louver import (  # noqa: F401
+    AttentionResult,
+    BuildConfig,
+    CacheQueryResult,
+    FilterAlgo,
+    LouverCache,
+    LouverLayer,
+    QueryRequest,
+    QueryStats,
+    brute_force_range,
+    lse_merge,
+    sparse_attention,
+)
+
+__all__ = [
+    "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
+    "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
+]

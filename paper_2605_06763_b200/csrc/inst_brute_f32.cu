@@ -1,0 +1,6 @@
+// Query-kernel instantiations: T=float, mode=kBrute, DP in {64,128,256}, G in {1,2,4,8}.
+#include "louver_dispatch.h"
+
+namespace lvk {
+LVK_DEFINE_LAUNCH_ALL(float, kBrute)
+}  // namespace lvk

@@ -1,0 +1,791 @@
+// C ABI of the B200 Louver hot path (include/louver_b200.h): context/arena
+// management, host<->device staging, and kernel launches. No CPU compute path:
+// every score, bound, selection and softmax runs in the kernels of
+// louver_kernels.cuh / louver_aux.cuh.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "louver_aux.cuh"
+#include "louver_b200.h"
+#include "louver_dispatch.h"
+
+using lvk::Counters;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define LV_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(LV_ERUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+int pad_dim(int d) { return d <= 64 ? 64 : (d <= 128 ? 128 : 256); }
+int esize(int dtype) { return dtype == LV_BF16 ? 2 : 4; }
+int ilog2(int x) {
+    int l = 0;
+    while ((1 << l) < x) ++l;
+    return l;
+}
+
+struct Workspace {
+    float* partial = nullptr;  // [slots][splits][G][DP+2]
+    int* tickets = nullptr;    // [slots]
+    float* q = nullptr;        // [rows][DP]
+    float* out = nullptr;      // [rows][DP]
+    float* tau = nullptr;      // [rows]
+    float* part_out = nullptr; // [rows][DP+2]
+    int* counts = nullptr;     // [rows][4]
+};
+
+}  // namespace
+
+struct lv_ctx {
+    lv_config cfg{};
+    int DP = 0, G = 1, r = 1, r_log2 = 0, slots = 0, rows = 0;
+    long long cap = 0, cap_cells = 0, bits_words = 0;
+    int splits = 1, chunks_per_split = 1;
+    void* K = nullptr;
+    void* V = nullptr;
+    void* lo = nullptr;
+    void* hi = nullptr;
+    float* colmax = nullptr;
+    Counters* ctr = nullptr;
+    int* ins_ticket = nullptr;
+    void* ws_mem = nullptr;
+    size_t ws_bytes = 0;
+    // host mirrors of the device counters
+    long long n = 0, indexed = 0, flushes = 0;
+    std::mutex writer;
+};
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Carve a workspace into its parts; returns the total size.
+size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = base ? base + off : nullptr;
+        off = align256(off + bytes);
+        return p;
+    };
+    const size_t rows = (size_t)c->rows;
+    unsigned char* t = take(sizeof(int) * c->slots);
+    unsigned char* part = take(sizeof(float) * c->slots * (size_t)c->splits * c->G * (c->DP + 2));
+    unsigned char* q = take(sizeof(float) * rows * c->DP);
+    unsigned char* o = take(sizeof(float) * rows * c->DP);
+    unsigned char* tau = take(sizeof(float) * rows);
+    unsigned char* po = take(sizeof(float) * rows * (c->DP + 2));
+    unsigned char* cnt = take(sizeof(int) * rows * 4);
+    if (w) {
+        w->tickets = reinterpret_cast<int*>(t);
+        w->partial = reinterpret_cast<float*>(part);
+        w->q = reinterpret_cast<float*>(q);
+        w->out = reinterpret_cast<float*>(o);
+        w->tau = reinterpret_cast<float*>(tau);
+        w->part_out = reinterpret_cast<float*>(po);
+        w->counts = reinterpret_cast<int*>(cnt);
+    }
+    return off;
+}
+
+int validate(const lv_config* c) {
+    if (!c) return fail(LV_EINVAL, "lv_create: null config");
+    if (c->d < 1 || c->d > 256) return fail(LV_EINVAL, "KeyStore: 1 <= d <= 256 required");
+    if (c->n_kv_heads < 1 || c->batch < 1) return fail(LV_EINVAL, "lv_create: heads/batch >= 1");
+    if (c->group_size != 1 && c->group_size != 2 && c->group_size != 4 && c->group_size != 8)
+        return fail(LV_EINVAL, "lv_create: group_size must be 1, 2, 4 or 8");
+    if (c->dtype != LV_F32 && c->dtype != LV_BF16) return fail(LV_EINVAL, "lv_create: dtype");
+    // BuildConfig::validate (index.hpp:17-21)
+    if (c->S < 1) return fail(LV_EINVAL, "BuildConfig: S >= 1 required");
+    if (c->r < 1) return fail(LV_EINVAL, "BuildConfig: r >= 1 required");
+    if (c->S > c->d) return fail(LV_EINVAL, "BuildConfig: S <= d required");
+    if (c->grouping < 0 || c->grouping > 3 || c->enclosure < 0 || c->enclosure > 2)
+        return fail(LV_EINVAL, "BuildConfig: unknown grouping or enclosure");
+    if (c->buffer_capacity < 1)
+        return fail(LV_EINVAL, "LouverCache: buffer capacity >= 1 required");
+    if (c->capacity < 1) return fail(LV_EINVAL, "lv_create: capacity >= 1 required");
+    return LV_OK;
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void choose_splits(lv_ctx* c) {
+    const long long chunks = c->cap / lvk::kChunk;
+    long long cps = 1;
+    if (const char* e = std::getenv("LV_CHUNKS_PER_SPLIT")) {
+        cps = std::max(1LL, std::atoll(e));
+    } else {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long target = (long long)sms * 6;  // ~2 waves at 3 CTAs/SM
+        cps = std::max(1LL, (chunks * c->slots + target - 1) / target);
+    }
+    long long splits = (chunks + cps - 1) / cps;
+    while (splits > 1024) {
+        ++cps;
+        splits = (chunks + cps - 1) / cps;
+    }
+    c->chunks_per_split = (int)cps;
+    c->splits = (int)splits;
+}
+
+// Copy a [rows][d] fp32 array (host or device) into a [rows][DP] device array.
+int stage_rows(lv_ctx* c, float* dst, const float* src, int where, cudaStream_t st) {
+    const size_t d = c->cfg.d;
+    if (d != (size_t)c->DP) LV_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * c->rows * c->DP, st));
+    LV_CUDA(cudaMemcpy2DAsync(dst, sizeof(float) * c->DP, src, sizeof(float) * d, sizeof(float) * d,
+                              c->rows, where == LV_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              st));
+    return LV_OK;
+}
+
+template <typename T>
+int launch_summaries_t(lv_ctx* c, long long cell_begin, long long cell_end, long long n,
+                       cudaStream_t st) {
+    const int CB = c->DP > 128 ? 16 : 32;
+    const long long ncell = cell_end - cell_begin;
+    if (ncell <= 0) return LV_OK;
+    dim3 grid((unsigned)((ncell + CB - 1) / CB), (unsigned)c->slots);
+    T* K = reinterpret_cast<T*>(c->K);
+    T* lo = reinterpret_cast<T*>(c->lo);
+    T* hi = reinterpret_cast<T*>(c->hi);
+    switch (c->DP) {
+        case 64:
+            lvk::summarize_kernel<T, 64><<<grid, 256, 0, st>>>(K, lo, hi, c->colmax, c->cap, c->cap_cells,
+                                                              c->r_log2, n, cell_begin, cell_end);
+            break;
+        case 128:
+            lvk::summarize_kernel<T, 128><<<grid, 256, 0, st>>>(K, lo, hi, c->colmax, c->cap, c->cap_cells,
+                                                               c->r_log2, n, cell_begin, cell_end);
+            break;
+        default:
+            lvk::summarize_kernel<T, 256><<<grid, 256, 0, st>>>(K, lo, hi, c->colmax, c->cap, c->cap_cells,
+                                                               c->r_log2, n, cell_begin, cell_end);
+    }
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int launch_summaries(lv_ctx* c, long long cell_begin, long long cell_end, long long n,
+                     cudaStream_t st) {
+    return c->cfg.dtype == LV_BF16
+               ? launch_summaries_t<__nv_bfloat16>(c, cell_begin, cell_end, n, st)
+               : launch_summaries_t<float>(c, cell_begin, cell_end, n, st);
+}
+
+template <typename S_, typename T>
+int launch_convert(lv_ctx* c, const void* src, void* dst, long long n, long long first,
+                   cudaStream_t st) {
+    const long long total = (long long)c->slots * n * c->DP;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    lvk::convert_rows_kernel<S_, T><<<blocks, 256, 0, st>>>(
+        reinterpret_cast<const S_*>(src), reinterpret_cast<T*>(dst), c->slots, n, c->cfg.d, c->DP,
+        c->cap, first);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int convert_into(lv_ctx* c, const void* src_dev, int src_dtype, void* arena, long long n,
+                 long long first, cudaStream_t st) {
+    const bool bf = c->cfg.dtype == LV_BF16;
+    if (src_dtype == LV_F32)
+        return bf ? launch_convert<float, __nv_bfloat16>(c, src_dev, arena, n, first, st)
+                  : launch_convert<float, float>(c, src_dev, arena, n, first, st);
+    if (!bf) return fail(LV_EINVAL, "bf16 source needs a bf16 cache");
+    return launch_convert<__nv_bfloat16, __nv_bfloat16>(c, src_dev, arena, n, first, st);
+}
+
+int sync_if_host(int where, cudaStream_t st) {
+    if (where == LV_HOST) LV_CUDA(cudaStreamSynchronize(st));
+    return LV_OK;
+}
+
+int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev, long long limit,
+                     float scale, int strict, Workspace& w, float* out, float* part_out,
+                     unsigned* bits, int* counts, unsigned long long* totals, cudaStream_t st) {
+    lvk::QueryParams p{};
+    p.K = c->K;
+    p.V = c->V;
+    p.lo = c->lo;
+    p.hi = c->hi;
+    p.colmax = c->colmax;
+    p.q = qdev;
+    p.tau = taudev;
+    p.ctr = c->ctr;
+    p.cap = c->cap;
+    p.cap_cells = c->cap_cells;
+    p.limit = limit;
+    p.r_log2 = c->r_log2;
+    p.chunks_per_split = c->chunks_per_split;
+    p.splits = c->splits;
+    p.strict = strict;
+    p.d_true = c->cfg.d;
+    p.scale = scale != 0.0f ? scale : (float)(1.0 / std::sqrt((double)c->cfg.d));
+    p.partial_ws = w.partial;
+    p.tickets = w.tickets;
+    p.out = out;
+    p.partial_out = part_out;
+    p.bits = bits;
+    p.bits_words = c->bits_words;
+    p.counts = counts;
+    p.totals = totals;
+    dim3 grid((unsigned)c->splits, (unsigned)c->slots);
+    const cudaError_t e = lvk::launch_query(c->cfg.dtype, c->DP, c->G, mode, p, grid, st);
+    if (e != cudaSuccess) return fail(LV_ERUNTIME, std::string("query kernel: ") + cudaGetErrorString(e));
+    return LV_OK;
+}
+
+}  // namespace
+
+namespace lvk {
+
+int query_smem_bytes(int dtype, int DP, int G) {
+#define LVK_SM(T)                                                   \
+    switch (DP * 16 + G) {                                          \
+        case 64 * 16 + 1: return Geo<T, 64, 1>::SMEM;               \
+        case 64 * 16 + 2: return Geo<T, 64, 2>::SMEM;               \
+        case 64 * 16 + 4: return Geo<T, 64, 4>::SMEM;               \
+        case 64 * 16 + 8: return Geo<T, 64, 8>::SMEM;               \
+        case 128 * 16 + 1: return Geo<T, 128, 1>::SMEM;             \
+        case 128 * 16 + 2: return Geo<T, 128, 2>::SMEM;             \
+        case 128 * 16 + 4: return Geo<T, 128, 4>::SMEM;             \
+        case 128 * 16 + 8: return Geo<T, 128, 8>::SMEM;             \
+        case 256 * 16 + 1: return Geo<T, 256, 1>::SMEM;             \
+        case 256 * 16 + 2: return Geo<T, 256, 2>::SMEM;             \
+        case 256 * 16 + 4: return Geo<T, 256, 4>::SMEM;             \
+        case 256 * 16 + 8: return Geo<T, 256, 8>::SMEM;             \
+    }
+    if (dtype == LV_BF16) {
+        LVK_SM(__nv_bfloat16)
+    } else {
+        LVK_SM(float)
+    }
+#undef LVK_SM
+    return -1;
+}
+
+cudaError_t launch_query(int dtype, int DP, int G, int mode, const QueryParams& p, dim3 grid,
+                         cudaStream_t st) {
+#define LVK_G(T, D, M)                                               \
+    switch (G) {                                                     \
+        case 1: return launch_query_t<T, D, 1, M>(p, grid, st);      \
+        case 2: return launch_query_t<T, D, 2, M>(p, grid, st);      \
+        case 4: return launch_query_t<T, D, 4, M>(p, grid, st);      \
+        case 8: return launch_query_t<T, D, 8, M>(p, grid, st);      \
+    }                                                                \
+    break;
+#define LVK_D(T, M)                    \
+    switch (DP) {                      \
+        case 64: LVK_G(T, 64, M)       \
+        case 128: LVK_G(T, 128, M)     \
+        case 256: LVK_G(T, 256, M)     \
+    }                                  \
+    break;
+#define LVK_M(T)                       \
+    switch (mode) {                    \
+        case kQuery: LVK_D(T, kQuery)  \
+        case kBrute: LVK_D(T, kBrute)  \
+        case kDense: LVK_D(T, kDense)  \
+    }
+    if (dtype == LV_BF16) {
+        LVK_M(__nv_bfloat16)
+    } else {
+        LVK_M(float)
+    }
+#undef LVK_G
+#undef LVK_D
+#undef LVK_M
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace lvk
+
+extern "C" {
+
+const char* lv_last_error(void) { return g_err.c_str(); }
+
+const char* lv_build_info(void) { return "louver_b200 0.1 sm_100a"; }
+
+int lv_create(const lv_config* cfg, lv_ctx** out) {
+    if (!out) return fail(LV_EINVAL, "lv_create: null out");
+    *out = nullptr;
+    if (int rc = validate(cfg)) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(LV_ENODEV, "lv_create: no CUDA device (the Louver hot path has no CPU fallback)");
+    auto* c = new lv_ctx();
+    c->cfg = *cfg;
+    c->DP = pad_dim(cfg->d);
+    c->G = cfg->group_size;
+    c->r = 1 << ilog2(std::min(cfg->r, 64));
+    c->r_log2 = ilog2(c->r);
+    c->slots = cfg->batch * cfg->n_kv_heads;
+    c->rows = c->slots * c->G;
+    c->cap = (cfg->capacity + lvk::kChunk - 1) / lvk::kChunk * lvk::kChunk;
+    c->cap_cells = c->cap / c->r;
+    c->bits_words = c->cap / 32;
+    choose_splits(c);
+    const size_t es = esize(cfg->dtype);
+    const size_t kv_bytes = (size_t)c->slots * c->cap * c->DP * es;
+    const size_t sum_bytes = (size_t)c->slots * c->DP * c->cap_cells * es;
+    auto cleanup = [&](const char* what, cudaError_t e) {
+        lv_destroy(c);
+        return fail(LV_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->K, kv_bytes)) != cudaSuccess) return cleanup("alloc K", e);
+    if ((e = cudaMalloc(&c->V, kv_bytes)) != cudaSuccess) return cleanup("alloc V", e);
+    if ((e = cudaMalloc(&c->lo, sum_bytes)) != cudaSuccess) return cleanup("alloc lo", e);
+    if ((e = cudaMalloc(&c->hi, sum_bytes)) != cudaSuccess) return cleanup("alloc hi", e);
+    if ((e = cudaMalloc(&c->colmax, sizeof(float) * c->slots * c->DP)) != cudaSuccess)
+        return cleanup("alloc colmax", e);
+    if ((e = cudaMalloc(&c->ctr, sizeof(Counters))) != cudaSuccess) return cleanup("alloc ctr", e);
+    if ((e = cudaMalloc(&c->ins_ticket, sizeof(int))) != cudaSuccess) return cleanup("alloc ticket", e);
+    c->ws_bytes = carve(c, nullptr, nullptr);
+    if ((e = cudaMalloc(&c->ws_mem, c->ws_bytes)) != cudaSuccess) return cleanup("alloc ws", e);
+    cudaMemset(c->K, 0, kv_bytes);
+    cudaMemset(c->V, 0, kv_bytes);
+    cudaMemset(c->colmax, 0, sizeof(float) * c->slots * c->DP);
+    cudaMemset(c->ctr, 0, sizeof(Counters));
+    cudaMemset(c->ins_ticket, 0, sizeof(int));
+    cudaMemset(c->ws_mem, 0, c->ws_bytes);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup("init", e);
+    *out = c;
+    return LV_OK;
+}
+
+int lv_destroy(lv_ctx* c) {
+    if (!c) return LV_OK;
+    cudaFree(c->K);
+    cudaFree(c->V);
+    cudaFree(c->lo);
+    cudaFree(c->hi);
+    cudaFree(c->colmax);
+    cudaFree(c->ctr);
+    cudaFree(c->ins_ticket);
+    cudaFree(c->ws_mem);
+    delete c;
+    return LV_OK;
+}
+
+size_t lv_query_workspace_bytes(const lv_ctx* c) { return c ? c->ws_bytes : 0; }
+int64_t lv_bitmap_words(const lv_ctx* c) { return c ? c->bits_words : 0; }
+int64_t lv_n(const lv_ctx* c) { return c->n; }
+int64_t lv_indexed_count(const lv_ctx* c) { return c->indexed; }
+int64_t lv_pending_count(const lv_ctx* c) { return c->n - c->indexed; }
+int64_t lv_flush_count(const lv_ctx* c) { return c->flushes; }
+
+int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
+    if (!c) return fail(LV_EINVAL, "lv_reserve: null context");
+    std::lock_guard<std::mutex> lock(c->writer);
+    if (capacity <= c->cfg.capacity) return LV_OK;
+    cudaStream_t st = S(stream);
+    LV_CUDA(cudaStreamSynchronize(st));
+    const long long ncap = (capacity + lvk::kChunk - 1) / lvk::kChunk * lvk::kChunk;
+    const long long ncells = ncap / c->r;
+    const size_t es = esize(c->cfg.dtype);
+    const size_t kv_bytes = (size_t)c->slots * ncap * c->DP * es;
+    const size_t sum_bytes = (size_t)c->slots * c->DP * ncells * es;
+    void *K = nullptr, *V = nullptr, *lo = nullptr, *hi = nullptr, *ws = nullptr;
+    auto undo = [&](cudaError_t e) {
+        cudaFree(K);
+        cudaFree(V);
+        cudaFree(lo);
+        cudaFree(hi);
+        cudaFree(ws);
+        return fail(LV_ERUNTIME, std::string("lv_reserve: ") + cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&K, kv_bytes)) != cudaSuccess) return undo(e);
+    if ((e = cudaMalloc(&V, kv_bytes)) != cudaSuccess) return undo(e);
+    if ((e = cudaMalloc(&lo, sum_bytes)) != cudaSuccess) return undo(e);
+    if ((e = cudaMalloc(&hi, sum_bytes)) != cudaSuccess) return undo(e);
+    cudaMemset(K, 0, kv_bytes);
+    cudaMemset(V, 0, kv_bytes);
+    // rows keep their ids: [slot][cap][DP] -> [slot][ncap][DP]; [slot][DP][cells] likewise
+    const size_t rowb = (size_t)c->cap * c->DP * es;
+    if ((e = cudaMemcpy2D(K, (size_t)ncap * c->DP * es, c->K, rowb, rowb, c->slots,
+                          cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
+    if ((e = cudaMemcpy2D(V, (size_t)ncap * c->DP * es, c->V, rowb, rowb, c->slots,
+                          cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
+    const size_t cellb = (size_t)c->cap_cells * es;
+    if ((e = cudaMemcpy2D(lo, (size_t)ncells * es, c->lo, cellb, cellb, (size_t)c->slots * c->DP,
+                          cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
+    if ((e = cudaMemcpy2D(hi, (size_t)ncells * es, c->hi, cellb, cellb, (size_t)c->slots * c->DP,
+                          cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
+    lv_ctx probe_geo;  // geometry for the new capacity's workspace
+    probe_geo.cfg = c->cfg;
+    probe_geo.DP = c->DP;
+    probe_geo.G = c->G;
+    probe_geo.slots = c->slots;
+    probe_geo.rows = c->rows;
+    probe_geo.cap = ncap;
+    choose_splits(&probe_geo);
+    const size_t wsb = carve(&probe_geo, nullptr, nullptr);
+    if ((e = cudaMalloc(&ws, wsb)) != cudaSuccess) return undo(e);
+    cudaMemset(ws, 0, wsb);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return undo(e);
+    cudaFree(c->K);
+    cudaFree(c->V);
+    cudaFree(c->lo);
+    cudaFree(c->hi);
+    cudaFree(c->ws_mem);
+    c->K = K;
+    c->V = V;
+    c->lo = lo;
+    c->hi = hi;
+    c->ws_mem = ws;
+    c->ws_bytes = wsb;
+    c->cap = ncap;
+    c->cap_cells = ncells;
+    c->bits_words = ncap / 32;
+    c->splits = probe_geo.splits;
+    c->chunks_per_split = probe_geo.chunks_per_split;
+    c->cfg.capacity = capacity;
+    return LV_OK;
+}
+
+int lv_build(lv_ctx* c, const void* K, const void* V, int64_t n, int src_dtype, int where,
+             void* stream) {
+    if (!c) return fail(LV_EINVAL, "lv_build: null context");
+    std::lock_guard<std::mutex> lock(c->writer);
+    if (n < 0 || n > c->cfg.capacity) return fail(LV_ERANGE, "lv_build: n exceeds capacity");
+    if (n > 0 && (!K || !V)) return fail(LV_EINVAL, "lv_build: null K/V");
+    if (src_dtype != LV_F32 && src_dtype != LV_BF16) return fail(LV_EINVAL, "lv_build: src dtype");
+    cudaStream_t st = S(stream);
+    const size_t src_bytes = (size_t)c->slots * n * c->cfg.d * esize(src_dtype);
+    LV_CUDA(cudaMemsetAsync(c->colmax, 0, sizeof(float) * c->slots * c->DP, st));
+    if (n > 0) {
+        const void* ksrc = K;
+        const void* vsrc = V;
+        void* tmp = nullptr;
+        if (where == LV_HOST) {
+            LV_CUDA(cudaMallocAsync(&tmp, 2 * src_bytes, st));
+            LV_CUDA(cudaMemcpyAsync(tmp, K, src_bytes, cudaMemcpyHostToDevice, st));
+            LV_CUDA(cudaMemcpyAsync((char*)tmp + src_bytes, V, src_bytes, cudaMemcpyHostToDevice, st));
+            ksrc = tmp;
+            vsrc = (char*)tmp + src_bytes;
+        }
+        int rc = convert_into(c, ksrc, src_dtype, c->K, n, 0, st);
+        if (!rc) rc = convert_into(c, vsrc, src_dtype, c->V, n, 0, st);
+        if (tmp) cudaFreeAsync(tmp, st);
+        if (rc) return rc;
+        if (int rc2 = launch_summaries(c, 0, (n + c->r - 1) / c->r, n, st)) return rc2;
+    }
+    Counters h{n, n, 0, 0};
+    LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    LV_CUDA(cudaStreamSynchronize(st));
+    c->n = n;
+    c->indexed = n;
+    c->flushes = 0;
+    return LV_OK;
+}
+
+int lv_push_key(lv_ctx* c, const void* k, const void* v, int src_dtype, int where, void* stream) {
+    if (!c || !k || !v) return fail(LV_EINVAL, "lv_push_key: null argument");
+    std::lock_guard<std::mutex> lock(c->writer);
+    if (c->n >= c->cfg.capacity) return fail(LV_ERANGE, "lv_push_key: arena capacity exhausted");
+    if (src_dtype != LV_F32 && !(src_dtype == LV_BF16 && c->cfg.dtype == LV_BF16))
+        return fail(LV_EINVAL, "lv_push_key: unsupported source dtype");
+    cudaStream_t st = S(stream);
+    const size_t bytes = (size_t)c->slots * c->cfg.d * esize(src_dtype);
+    const void* kd = k;
+    const void* vd = v;
+    void* tmp = nullptr;
+    if (where == LV_HOST) {
+        LV_CUDA(cudaMallocAsync(&tmp, 2 * bytes, st));
+        LV_CUDA(cudaMemcpyAsync(tmp, k, bytes, cudaMemcpyHostToDevice, st));
+        LV_CUDA(cudaMemcpyAsync((char*)tmp + bytes, v, bytes, cudaMemcpyHostToDevice, st));
+        kd = tmp;
+        vd = (char*)tmp + bytes;
+    }
+    const int threads = c->DP;
+    const long long B = c->cfg.buffer_capacity;
+    if (c->cfg.dtype == LV_BF16) {
+        auto* K = reinterpret_cast<__nv_bfloat16*>(c->K);
+        auto* Vv = reinterpret_cast<__nv_bfloat16*>(c->V);
+        auto* lo = reinterpret_cast<__nv_bfloat16*>(c->lo);
+        auto* hi = reinterpret_cast<__nv_bfloat16*>(c->hi);
+        if (src_dtype == LV_F32)
+            lvk::insert_kernel<float, __nv_bfloat16><<<c->slots, threads, 0, st>>>(
+                (const float*)kd, (const float*)vd, K, Vv, lo, hi, c->colmax, c->ctr, c->ins_ticket,
+                c->cfg.d, c->DP, c->cap, c->cap_cells, c->r_log2, B, c->slots);
+        else
+            lvk::insert_kernel<__nv_bfloat16, __nv_bfloat16><<<c->slots, threads, 0, st>>>(
+                (const __nv_bfloat16*)kd, (const __nv_bfloat16*)vd, K, Vv, lo, hi, c->colmax, c->ctr,
+                c->ins_ticket, c->cfg.d, c->DP, c->cap, c->cap_cells, c->r_log2, B, c->slots);
+    } else {
+        lvk::insert_kernel<float, float><<<c->slots, threads, 0, st>>>(
+            (const float*)kd, (const float*)vd, (float*)c->K, (float*)c->V, (float*)c->lo,
+            (float*)c->hi, c->colmax, c->ctr, c->ins_ticket, c->cfg.d, c->DP, c->cap, c->cap_cells,
+            c->r_log2, B, c->slots);
+    }
+    LV_CUDA(cudaGetLastError());
+    if (tmp) LV_CUDA(cudaFreeAsync(tmp, st));
+    if (int rc = sync_if_host(where, st)) return rc;
+    c->n += 1;
+    if (c->n - c->indexed >= B) {
+        c->indexed = c->n;
+        c->flushes += 1;
+    }
+    return LV_OK;
+}
+
+int lv_sync_counters(lv_ctx* c, void* stream) {
+    if (!c) return fail(LV_EINVAL, "lv_sync_counters: null context");
+    Counters h{};
+    LV_CUDA(cudaMemcpyAsync(&h, c->ctr, sizeof(h), cudaMemcpyDeviceToHost, S(stream)));
+    LV_CUDA(cudaStreamSynchronize(S(stream)));
+    c->n = h.n;
+    c->indexed = h.indexed;
+    c->flushes = h.flushes;
+    return LV_OK;
+}
+
+int lv_flush(lv_ctx* c, void* stream) {
+    if (!c) return fail(LV_EINVAL, "lv_flush: null context");
+    std::lock_guard<std::mutex> lock(c->writer);
+    if (c->n == c->indexed) return LV_EMPTY;  // cache.cpp:14
+    // The summaries already cover every stored key (lv_push_key folds each key
+    // into its cell), so folding the buffer into the index is a counter move.
+    Counters h{c->n, c->n, c->flushes + 1, 0};
+    LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)));
+    LV_CUDA(cudaStreamSynchronize(S(stream)));
+    c->indexed = c->n;
+    c->flushes += 1;
+    return LV_OK;
+}
+
+int lv_query(lv_ctx* c, const lv_query_args* a) {
+    if (!c || !a || !a->q || !a->tau) return fail(LV_EINVAL, "lv_query: null argument");
+    cudaStream_t st = S(a->stream);
+    Workspace w;
+    carve(c, reinterpret_cast<unsigned char*>(a->workspace ? a->workspace : c->ws_mem), &w);
+    const bool direct = a->where == LV_DEVICE && c->cfg.d == c->DP;
+    const float* qd = a->q;
+    const float* taud = a->tau;
+    if (!direct) {
+        if (int rc = stage_rows(c, w.q, a->q, a->where, st)) return rc;
+        qd = w.q;
+    }
+    if (a->where == LV_HOST) {
+        LV_CUDA(cudaMemcpyAsync(w.tau, a->tau, sizeof(float) * c->rows, cudaMemcpyHostToDevice, st));
+        taud = w.tau;
+    }
+    float* outd = direct ? a->out : (a->out ? w.out : nullptr);
+    float* pod = (a->partial && direct) ? a->partial : (a->partial ? w.part_out : nullptr);
+    int* cntd = a->counts ? (a->where == LV_DEVICE ? a->counts : w.counts) : nullptr;
+    if (cntd) LV_CUDA(cudaMemsetAsync(cntd, 0, sizeof(int) * c->rows * 4, st));
+    if (a->totals) LV_CUDA(cudaMemsetAsync(a->totals, 0, sizeof(uint64_t) * 4, st));
+    if (a->sel_bits)
+        LV_CUDA(cudaMemsetAsync(a->sel_bits, 0, sizeof(uint32_t) * c->rows * c->bits_words, st));
+    if (int rc = run_query_kernel(c, lvk::kQuery, qd, taud, 0, a->scale, a->strict, w, outd, pod,
+                                  a->sel_bits, cntd, reinterpret_cast<unsigned long long*>(a->totals),
+                                  st))
+        return rc;
+    const cudaMemcpyKind kind = a->where == LV_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (a->out && !direct)
+        LV_CUDA(cudaMemcpy2DAsync(a->out, sizeof(float) * c->cfg.d, w.out, sizeof(float) * c->DP,
+                                  sizeof(float) * c->cfg.d, c->rows, kind, st));
+    if (a->partial && !direct) {
+        // (m, l, o[d]) rows of the caller's d+2 width
+        LV_CUDA(cudaMemcpy2DAsync(a->partial, sizeof(float) * (c->cfg.d + 2), w.part_out,
+                                  sizeof(float) * (c->DP + 2), sizeof(float) * (c->cfg.d + 2), c->rows,
+                                  kind, st));
+    }
+    if (a->counts && a->where == LV_HOST)
+        LV_CUDA(cudaMemcpyAsync(a->counts, w.counts, sizeof(int) * c->rows * 4, cudaMemcpyDeviceToHost, st));
+    return sync_if_host(a->where, st);
+}
+
+int lv_dense_decode(lv_ctx* c, const float* q, float scale, int where, float* out, float* partial,
+                    void* stream) {
+    if (!c || !q) return fail(LV_EINVAL, "lv_dense_decode: null argument");
+    cudaStream_t st = S(stream);
+    Workspace w;
+    carve(c, reinterpret_cast<unsigned char*>(c->ws_mem), &w);
+    const bool direct = where == LV_DEVICE && c->cfg.d == c->DP;
+    const float* qd = q;
+    if (!direct) {
+        if (int rc = stage_rows(c, w.q, q, where, st)) return rc;
+        qd = w.q;
+    }
+    float* outd = direct ? out : (out ? w.out : nullptr);
+    float* pod = (partial && direct) ? partial : (partial ? w.part_out : nullptr);
+    if (int rc = run_query_kernel(c, lvk::kDense, qd, nullptr, 0, scale, 0, w, outd, pod, nullptr,
+                                  nullptr, nullptr, st))
+        return rc;
+    const cudaMemcpyKind kind = where == LV_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (out && !direct)
+        LV_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * c->cfg.d, w.out, sizeof(float) * c->DP,
+                                  sizeof(float) * c->cfg.d, c->rows, kind, st));
+    if (partial && !direct)
+        LV_CUDA(cudaMemcpy2DAsync(partial, sizeof(float) * (c->cfg.d + 2), w.part_out,
+                                  sizeof(float) * (c->DP + 2), sizeof(float) * (c->cfg.d + 2), c->rows,
+                                  kind, st));
+    return sync_if_host(where, st);
+}
+
+int lv_brute_force_range(lv_ctx* c, const float* q, const float* tau, int64_t limit, int where,
+                         uint32_t* sel_bits, void* stream) {
+    if (!c || !q || !tau || !sel_bits) return fail(LV_EINVAL, "lv_brute_force_range: null argument");
+    if (limit < 0 || limit > c->n) return fail(LV_EINVAL, "brute_force_range: limit > n");
+    cudaStream_t st = S(stream);
+    Workspace w;
+    carve(c, reinterpret_cast<unsigned char*>(c->ws_mem), &w);
+    const float* qd = q;
+    const float* taud = tau;
+    if (!(where == LV_DEVICE && c->cfg.d == c->DP)) {
+        if (int rc = stage_rows(c, w.q, q, where, st)) return rc;
+        qd = w.q;
+    }
+    if (where == LV_HOST) {
+        LV_CUDA(cudaMemcpyAsync(w.tau, tau, sizeof(float) * c->rows, cudaMemcpyHostToDevice, st));
+        taud = w.tau;
+    }
+    LV_CUDA(cudaMemsetAsync(sel_bits, 0, sizeof(uint32_t) * c->rows * c->bits_words, st));
+    if (int rc = run_query_kernel(c, lvk::kBrute, qd, taud, limit, 0.0f, 0, w, nullptr, nullptr,
+                                  sel_bits, nullptr, nullptr, st))
+        return rc;
+    return sync_if_host(where, st);
+}
+
+int lv_bitmap_to_ids(const uint32_t* bits, int64_t words, int64_t rows, int64_t limit, uint32_t* ids,
+                     int64_t ids_stride, int32_t* count, void* stream) {
+    if (!bits || !ids || !count || rows < 0 || limit > words * 32)
+        return fail(LV_EINVAL, "lv_bitmap_to_ids: bad arguments");
+    if (rows == 0) return LV_OK;
+    lvk::bitmap_ids_kernel<<<(unsigned)rows, 256, 0, S(stream)>>>(bits, words, limit, ids, ids_stride,
+                                                                  count);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream) {
+    if (!partials || !out || P < 1 || P > 64 || rows < 0 || d < 1)
+        return fail(LV_EINVAL, "lv_lse_merge: bad arguments");
+    if (rows == 0) return LV_OK;
+    lvk::lse_merge_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(partials, P, rows, d, d + 2, out, d,
+                                                                 nullptr);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_sparse_attention(lv_ctx* c, int slot, const uint32_t* buffer_ids, int64_t nbuf,
+                        const uint32_t* selected_ids, int64_t nsel, const float* q, float scale,
+                        int where, float* out, float* weights, int64_t* ntok, void* stream) {
+    if (!c || !q || !out) return fail(LV_EINVAL, "sparse_attention: null argument");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "sparse_attention: slot out of range");
+    if (nbuf < 0 || nsel < 0) return fail(LV_EINVAL, "sparse_attention: negative count");
+    cudaStream_t st = S(stream);
+    // tokens = sort ∪ unique(selected ∪ buffer)  (query.cpp:342-345)
+    std::vector<uint32_t> tok;
+    tok.reserve((size_t)(nbuf + nsel));
+    auto gather = [&](const uint32_t* ids, int64_t cnt) -> int {
+        if (cnt == 0) return LV_OK;
+        if (!ids) return fail(LV_EINVAL, "sparse_attention: null id list");
+        const size_t at = tok.size();
+        tok.resize(at + cnt);
+        if (where == LV_HOST) {
+            std::memcpy(tok.data() + at, ids, sizeof(uint32_t) * cnt);
+        } else {
+            LV_CUDA(cudaMemcpyAsync(tok.data() + at, ids, sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost, st));
+            LV_CUDA(cudaStreamSynchronize(st));
+        }
+        return LV_OK;
+    };
+    if (int rc = gather(selected_ids, nsel)) return rc;
+    if (int rc = gather(buffer_ids, nbuf)) return rc;
+    std::sort(tok.begin(), tok.end());
+    tok.erase(std::unique(tok.begin(), tok.end()), tok.end());
+    if (ntok) *ntok = (int64_t)tok.size();
+    if (tok.empty()) return LV_EMPTY;
+    if ((long long)tok.back() >= c->n) return fail(LV_ERANGE, "sparse_attention: id out of range");
+    const long long nt = (long long)tok.size();
+    const int per = (int)std::max<long long>(256, (nt + 63) / 64);
+    const int P = (int)((nt + per - 1) / per);
+    const size_t bytes = align256(sizeof(uint32_t) * nt) + align256(sizeof(float) * nt) +
+                         align256(sizeof(float) * P * (c->DP + 2)) + align256(sizeof(float) * c->DP * 2) +
+                         align256(sizeof(float) * 2);
+    unsigned char* mem = nullptr;
+    LV_CUDA(cudaMallocAsync((void**)&mem, bytes, st));
+    unsigned* dids = reinterpret_cast<unsigned*>(mem);
+    float* scores = reinterpret_cast<float*>(mem + align256(sizeof(uint32_t) * nt));
+    float* part = reinterpret_cast<float*>((unsigned char*)scores + align256(sizeof(float) * nt));
+    float* qpad = reinterpret_cast<float*>((unsigned char*)part + align256(sizeof(float) * P * (c->DP + 2)));
+    float* opad = qpad + c->DP;
+    float* ml = reinterpret_cast<float*>((unsigned char*)qpad + align256(sizeof(float) * c->DP * 2));
+    LV_CUDA(cudaMemcpyAsync(dids, tok.data(), sizeof(uint32_t) * nt, cudaMemcpyHostToDevice, st));
+    LV_CUDA(cudaMemsetAsync(qpad, 0, sizeof(float) * c->DP, st));
+    LV_CUDA(cudaMemcpyAsync(qpad, q, sizeof(float) * c->cfg.d,
+                            where == LV_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    const float sc = scale != 0.0f ? scale : (float)(1.0 / std::sqrt((double)c->cfg.d));
+    const size_t es = esize(c->cfg.dtype);
+    const void* Ks = (const unsigned char*)c->K + (size_t)slot * c->cap * c->DP * es;
+    const void* Vs = (const unsigned char*)c->V + (size_t)slot * c->cap * c->DP * es;
+    const unsigned tb = (unsigned)((nt + 127) / 128);
+#define LV_ATT(T, D)                                                                                  \
+    lvk::token_scores_kernel<T, D><<<tb, 128, 0, st>>>((const T*)Ks, dids, nt, qpad, sc, scores);     \
+    lvk::token_partials_kernel<T, D><<<P, 128, 0, st>>>((const T*)Vs, dids, scores, nt, per, part);
+    if (c->cfg.dtype == LV_BF16) {
+        if (c->DP == 64) { LV_ATT(__nv_bfloat16, 64) } else if (c->DP == 128) { LV_ATT(__nv_bfloat16, 128) } else { LV_ATT(__nv_bfloat16, 256) }
+    } else {
+        if (c->DP == 64) { LV_ATT(float, 64) } else if (c->DP == 128) { LV_ATT(float, 128) } else { LV_ATT(float, 256) }
+    }
+#undef LV_ATT
+    lvk::lse_merge_kernel<<<1, 128, 0, st>>>(part, P, 1, c->DP, c->DP + 2, opad, c->DP, ml);
+    LV_CUDA(cudaGetLastError());
+    const cudaMemcpyKind kind = where == LV_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    LV_CUDA(cudaMemcpyAsync(out, opad, sizeof(float) * c->cfg.d, kind, st));
+    if (weights) {
+        lvk::token_weights_kernel<<<tb, 128, 0, st>>>(scores, nt, ml, scores);
+        LV_CUDA(cudaGetLastError());
+        LV_CUDA(cudaMemcpyAsync(weights, scores, sizeof(float) * nt, kind, st));
+    }
+    LV_CUDA(cudaFreeAsync(mem, st));
+    LV_CUDA(cudaStreamSynchronize(st));
+    return LV_OK;
+}
+
+int lv_read_rows(const lv_ctx* c, int slot, int64_t first, int64_t count, int which_v, float* out) {
+    if (!c || !out) return fail(LV_EINVAL, "lv_read_rows: null argument");
+    if (slot < 0 || slot >= c->slots || first < 0 || first + count > c->n)
+        return fail(LV_ERANGE, "lv_read_rows: range");
+    const size_t es = esize(c->cfg.dtype);
+    std::vector<unsigned char> buf((size_t)count * c->DP * es);
+    const unsigned char* src = (const unsigned char*)(which_v ? c->V : c->K) +
+                               ((size_t)slot * c->cap + first) * c->DP * es;
+    LV_CUDA(cudaMemcpy(buf.data(), src, buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < count; ++j)
+        for (int i = 0; i < c->cfg.d; ++i) {
+            const size_t at = (size_t)j * c->DP + i;
+            if (es == 4) {
+                std::memcpy(out + j * c->cfg.d + i, buf.data() + at * 4, 4);
+            } else {
+                uint16_t h;
+                std::memcpy(&h, buf.data() + at * 2, 2);
+                const uint32_t u = (uint32_t)h << 16;
+                std::memcpy(out + j * c->cfg.d + i, &u, 4);
+            }
+        }
+    return LV_OK;
+}
+
+}  // extern "C"

@@ -140,6 +140,10 @@ int lv_flush(lv_ctx* ctx, void* stream);
 
 int lv_query(lv_ctx* ctx, const lv_query_args* args);
 size_t lv_query_workspace_bytes(const lv_ctx* ctx);
+
+/* Device geometry: out[8] = {padded d, cell keys r, arena rows, cells per slot,
+ * query splits per slot, chunks per split, keys per chunk, query smem bytes}. */
+int lv_geometry(const lv_ctx* ctx, int64_t* out);
 int64_t lv_bitmap_words(const lv_ctx* ctx);
 
 /* Host mirrors of the device counters (uniform over slots). */

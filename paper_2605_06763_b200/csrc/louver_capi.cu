@@ -386,6 +386,19 @@ int lv_destroy(lv_ctx* c) {
 }
 
 size_t lv_query_workspace_bytes(const lv_ctx* c) { return c ? c->ws_bytes : 0; }
+
+int lv_geometry(const lv_ctx* c, int64_t* out) {
+    if (!c || !out) return fail(LV_EINVAL, "lv_geometry: null argument");
+    out[0] = c->DP;
+    out[1] = c->r;
+    out[2] = c->cap;
+    out[3] = c->cap_cells;
+    out[4] = c->splits;
+    out[5] = c->chunks_per_split;
+    out[6] = lvk::kChunk;
+    out[7] = lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
+    return LV_OK;
+}
 int64_t lv_bitmap_words(const lv_ctx* c) { return c ? c->bits_words : 0; }
 int64_t lv_n(const lv_ctx* c) { return c->n; }
 int64_t lv_indexed_count(const lv_ctx* c) { return c->indexed; }

@@ -370,6 +370,13 @@ class LouverLayer:
     def workspace_bytes(self) -> int:
         return int(self._ctx.lib.lv_query_workspace_bytes(self._ctx.h))
 
+    def geometry(self) -> dict:
+        g = np.zeros((8,), np.int64)
+        check(self._ctx.lib.lv_geometry(self._ctx.h, g.ctypes.data), "lv_geometry")
+        keys = ("dp", "cell_keys", "arena_rows", "cells", "splits", "chunks_per_split", "chunk_keys",
+                "smem_bytes")
+        return {k: int(v) for k, v in zip(keys, g)}
+
     def build(self, K, V, stream=None) -> None:
         """K, V: [batch][H_kv][n][d] fp32 or bf16 (numpy host or torch cuda)."""
         torch = _torch()

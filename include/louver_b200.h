@@ -144,6 +144,10 @@ size_t lv_query_workspace_bytes(const lv_ctx* ctx);
 /* Device geometry: out[8] = {padded d, cell keys r, arena rows, cells per slot,
  * query splits per slot, chunks per split, keys per chunk, query smem bytes}. */
 int lv_geometry(const lv_ctx* ctx, int64_t* out);
+
+/* Debug: while dev_buf != NULL, bf16 queries write 8 globaltimer stamps per
+ * CTA (grid order [slot][split]) into dev_buf [slots*splits][8]. */
+int lv_debug_trace(lv_ctx* ctx, int64_t* dev_buf);
 int64_t lv_bitmap_words(const lv_ctx* ctx);
 
 /* Host mirrors of the device counters (uniform over slots). */

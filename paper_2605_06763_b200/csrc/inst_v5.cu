@@ -1,0 +1,47 @@
+// v5 (bf16, flat warp-level) instantiations: DP in {64,128,256} x G in {1,2,4,8}.
+#include "louver_v5.cuh"
+
+namespace lvk5 {
+
+template <int DP, int G>
+static cudaError_t launch_t(const V5Params& vp, int slots, cudaStream_t st) {
+    static bool attr1 = false;
+    static int smem2_set = 0;
+    constexpr int smem1 = P5<DP, G>::SMEM;
+    const int smem2 = E5<DP, G>::smem(vp.tiles);
+    if (!attr1) {
+        cudaError_t e = cudaFuncSetAttribute(louver_probe_v5<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+        if (e != cudaSuccess) return e;
+        attr1 = true;
+    }
+    if (smem2 > smem2_set) {
+        cudaError_t e = cudaFuncSetAttribute(louver_exact_v5<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        if (e != cudaSuccess) return e;
+        smem2_set = smem2;
+    }
+    louver_probe_v5<DP, G><<<dim3((unsigned)vp.nbp, (unsigned)slots), kT, smem1, st>>>(vp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    louver_exact_v5<DP, G><<<dim3((unsigned)vp.nb, (unsigned)slots), kT, smem2, st>>>(vp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_query_v5(int DP, int G, const V5Params& vp, int slots, cudaStream_t st) {
+#define LV5_G(D)                                          \
+    switch (G) {                                          \
+        case 1: return launch_t<D, 1>(vp, slots, st);     \
+        case 2: return launch_t<D, 2>(vp, slots, st);     \
+        case 4: return launch_t<D, 4>(vp, slots, st);     \
+        case 8: return launch_t<D, 8>(vp, slots, st);     \
+    }                                                     \
+    break;
+    switch (DP) {
+        case 64: LV5_G(64)
+        case 128: LV5_G(128)
+        case 256: LV5_G(256)
+    }
+#undef LV5_G
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace lvk5

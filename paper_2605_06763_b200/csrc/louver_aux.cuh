@@ -36,7 +36,7 @@ __global__ void convert_rows_kernel(const S* __restrict__ src, T* __restrict__ d
 }
 
 // Cell AABBs for cells [cell_begin, cell_end) of every slot over keys [0, n):
-// lo/hi[slot][DP][cap_cells] = per-coordinate min/max of the cell's keys
+// summary row [slot][cell] = [hi (DP) | lo (DP)], per-coordinate max/min of the cell's keys
 // (exactly representable in T: they are stored key values). Also folds
 // max |k_c| into colmax[slot][DP]. One CTA = 32 cells (16 at DP=256) of one slot.
 template <typename T, int DP>
@@ -87,14 +87,14 @@ __global__ void __launch_bounds__(256) summarize_kernel(const T* __restrict__ K,
     atomicMax(reinterpret_cast<int*>(&cmax[2 * dp]), __float_as_int(am0));
     atomicMax(reinterpret_cast<int*>(&cmax[2 * dp + 1]), __float_as_int(am1));
     __syncthreads();
-    T* los = lo + (size_t)slot * DP * cap_cells;
-    T* his = hi + (size_t)slot * DP * cap_cells;
-    for (int i = tid; i < DP * CB; i += 256) {
-        const int c = i / CB, cl = i % CB;
+    // cell-major layout: one row per cell = [hi (DP) | lo (DP)]
+    (void)hi;
+    for (int i = tid; i < 2 * DP * CB; i += 256) {
+        const int cl = i / (2 * DP), e = i % (2 * DP);
         const long long cell = c0 + cl;
         if (cell < cell_end && (cell << r_log2) < n) {
-            los[(size_t)c * cap_cells + cell] = from_f<T>(slo[c][cl]);
-            his[(size_t)c * cap_cells + cell] = from_f<T>(shi[c][cl]);
+            const size_t at = ((size_t)slot * cap_cells + (size_t)cell) * 2 * DP + (size_t)e;
+            lo[at] = from_f<T>(e < DP ? shi[e][cl] : slo[e - DP][cl]);
         }
     }
     for (int c = tid; c < DP; c += 256)
@@ -123,8 +123,10 @@ __global__ void insert_kernel(const S* __restrict__ k, const S* __restrict__ v, 
         K[((size_t)slot * cap + pos) * DP + c] = kt;
         V[((size_t)slot * cap + pos) * DP + c] = from_f<T>(vx);
         const float kr = to_f<T>(kt);
-        T* lp = lo + ((size_t)slot * DP + c) * cap_cells + cell;
-        T* hp = hi + ((size_t)slot * DP + c) * cap_cells + cell;
+        // cell-major summary row [hi (DP) | lo (DP)]
+        T* hp = lo + ((size_t)slot * cap_cells + (size_t)cell) * 2 * DP + (size_t)c;
+        T* lp = hp + DP;
+        (void)hi;
         if (open) {
             *lp = kt;
             *hp = kt;

@@ -14,6 +14,8 @@
 #include "louver_aux.cuh"
 #include "louver_b200.h"
 #include "louver_dispatch.h"
+#include "louver_v2.cuh"
+#include "louver_v5.cuh"
 
 using lvk::Counters;
 
@@ -41,9 +43,15 @@ int ilog2(int x) {
     return l;
 }
 
+constexpr long long kCapAlign = 1024;  // arena rows per slot: a whole number of v2 units
+
 struct Workspace {
     float* partial = nullptr;  // [slots][splits][G][DP+2]
     int* tickets = nullptr;    // [slots]
+    float* gpart = nullptr;    // [slots][ngroups][G][DP+2] (v2 merge tree)
+    int* gtickets = nullptr;   // [slots][ngroups]
+    int* stickets = nullptr;   // [slots]
+    unsigned* cmask = nullptr; // [slots][units] survivor cells (v4 probe -> exact)
     float* q = nullptr;        // [rows][DP]
     float* out = nullptr;      // [rows][DP]
     float* tau = nullptr;      // [rows]
@@ -57,7 +65,8 @@ struct lv_ctx {
     lv_config cfg{};
     int DP = 0, G = 1, r = 1, r_log2 = 0, slots = 0, rows = 0;
     long long cap = 0, cap_cells = 0, bits_words = 0;
-    int splits = 1, chunks_per_split = 1;
+    int splits = 1, chunks_per_split = 1, ngroups = 1;
+    int nb = 1, nb_groups = 1, units = 1;  // v4: exact CTAs per slot, their merge groups, 512-key units
     void* K = nullptr;
     void* V = nullptr;
     void* lo = nullptr;
@@ -69,6 +78,7 @@ struct lv_ctx {
     size_t ws_bytes = 0;
     // host mirrors of the device counters
     long long n = 0, indexed = 0, flushes = 0;
+    long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     std::mutex writer;
 };
 
@@ -86,13 +96,23 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
     };
     const size_t rows = (size_t)c->rows;
     unsigned char* t = take(sizeof(int) * c->slots);
-    unsigned char* part = take(sizeof(float) * c->slots * (size_t)c->splits * c->G * (c->DP + 2));
+    const size_t nparts = (size_t)std::max(c->splits, c->nb);
+    unsigned char* part = take(sizeof(float) * c->slots * nparts * c->G * (c->DP + 2));
     unsigned char* q = take(sizeof(float) * rows * c->DP);
     unsigned char* o = take(sizeof(float) * rows * c->DP);
     unsigned char* tau = take(sizeof(float) * rows);
     unsigned char* po = take(sizeof(float) * rows * (c->DP + 2));
     unsigned char* cnt = take(sizeof(int) * rows * 4);
+    const size_t ngr = (size_t)std::max(c->ngroups, c->nb_groups);
+    unsigned char* gp = take(sizeof(float) * c->slots * ngr * c->G * (c->DP + 2));
+    unsigned char* gt = take(sizeof(int) * c->slots * ngr);
+    unsigned char* stk = take(sizeof(int) * c->slots);
+    unsigned char* cmk = take(sizeof(unsigned) * c->slots * (size_t)c->units);
     if (w) {
+        w->gpart = reinterpret_cast<float*>(gp);
+        w->gtickets = reinterpret_cast<int*>(gt);
+        w->stickets = reinterpret_cast<int*>(stk);
+        w->cmask = reinterpret_cast<unsigned*>(cmk);
         w->tickets = reinterpret_cast<int*>(t);
         w->partial = reinterpret_cast<float*>(part);
         w->q = reinterpret_cast<float*>(q);
@@ -126,6 +146,22 @@ int validate(const lv_config* c) {
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 void choose_splits(lv_ctx* c) {
+    if (c->cfg.dtype == LV_BF16) {  // v2 kernel: one CTA per fixed 1024-key unit
+        c->chunks_per_split = lvk2::kUnitChunks;
+        c->splits = (int)(c->cap / lvk2::kUnit);
+        c->ngroups = (c->splits + lvk2::kGroup - 1) / lvk2::kGroup;
+        c->units = (int)(c->cap / lvk::kChunk);
+        // v4 exact kernel: balanced rows, ~2 resident CTAs per SM in one wave
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        long long nb = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
+        if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
+        c->nb = (int)std::min<long long>(nb, 4096);
+        c->nb_groups = (c->nb + lvk5::kMG - 1) / lvk5::kMG;
+        return;
+    }
+    c->ngroups = 1;
     const long long chunks = c->cap / lvk::kChunk;
     long long cps = 1;
     if (const char* e = std::getenv("LV_CHUNKS_PER_SPLIT")) {
@@ -247,7 +283,35 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
     p.counts = counts;
     p.totals = totals;
     dim3 grid((unsigned)c->splits, (unsigned)c->slots);
-    const cudaError_t e = lvk::launch_query(c->cfg.dtype, c->DP, c->G, mode, p, grid, st);
+    cudaError_t e;
+    if (c->cfg.dtype == LV_BF16 && mode == lvk::kQuery) {
+        lvk5::V5Params v5{};
+        v5.p = p;
+        v5.p.splits = c->nb;
+        v5.sum = reinterpret_cast<const __nv_bfloat16*>(c->lo);
+        v5.cmask = reinterpret_cast<unsigned short*>(w.cmask);
+        v5.tiles = (int)(c->cap_cells / 16);
+        v5.nbp = c->nb;
+        v5.nb = c->nb;
+        v5.gpart = w.gpart;
+        v5.gtickets = w.gtickets;
+        v5.stickets = w.stickets;
+        v5.ngroups = c->nb_groups;
+        e = lvk5::launch_query_v5(c->DP, c->G, v5, c->slots, st);
+    } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
+        lvk2::V2Params vp{};
+        vp.p = p;
+        vp.sum = c->lo;
+        vp.gpart = w.gpart;
+        vp.gtickets = w.gtickets;
+        vp.stickets = w.stickets;
+        vp.ngroups = c->ngroups;
+        vp.mode_dense = mode == lvk::kDense ? 1 : 0;
+        vp.trace = c->trace;
+        e = lvk2::launch_query_v2(c->DP, c->G, vp, grid, st);
+    } else {
+        e = lvk::launch_query(c->cfg.dtype, c->DP, c->G, mode, p, grid, st);
+    }
     if (e != cudaSuccess) return fail(LV_ERUNTIME, std::string("query kernel: ") + cudaGetErrorString(e));
     return LV_OK;
 }
@@ -334,17 +398,19 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
     c->cfg = *cfg;
     c->DP = pad_dim(cfg->d);
     c->G = cfg->group_size;
-    c->r = 1 << ilog2(std::min(cfg->r, 64));
+    // device cells: contiguous, r rounded up to a power of two in [16, 64]
+    c->r = std::max(16, 1 << ilog2(std::min(cfg->r, 64)));
     c->r_log2 = ilog2(c->r);
     c->slots = cfg->batch * cfg->n_kv_heads;
     c->rows = c->slots * c->G;
-    c->cap = (cfg->capacity + lvk::kChunk - 1) / lvk::kChunk * lvk::kChunk;
+    c->cap = (cfg->capacity + kCapAlign - 1) / kCapAlign * kCapAlign;
     c->cap_cells = c->cap / c->r;
     c->bits_words = c->cap / 32;
     choose_splits(c);
     const size_t es = esize(cfg->dtype);
     const size_t kv_bytes = (size_t)c->slots * c->cap * c->DP * es;
-    const size_t sum_bytes = (size_t)c->slots * c->DP * c->cap_cells * es;
+    // blocked summaries [slot][chunk][lo|hi][DP][cells per chunk]
+    const size_t sum_bytes = 2 * (size_t)c->slots * c->DP * c->cap_cells * es;
     auto cleanup = [&](const char* what, cudaError_t e) {
         lv_destroy(c);
         return fail(LV_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
@@ -352,8 +418,8 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
     cudaError_t e;
     if ((e = cudaMalloc(&c->K, kv_bytes)) != cudaSuccess) return cleanup("alloc K", e);
     if ((e = cudaMalloc(&c->V, kv_bytes)) != cudaSuccess) return cleanup("alloc V", e);
-    if ((e = cudaMalloc(&c->lo, sum_bytes)) != cudaSuccess) return cleanup("alloc lo", e);
-    if ((e = cudaMalloc(&c->hi, sum_bytes)) != cudaSuccess) return cleanup("alloc hi", e);
+    if ((e = cudaMalloc(&c->lo, sum_bytes)) != cudaSuccess) return cleanup("alloc summaries", e);
+    c->hi = c->lo;  // lo and hi live in the same blocked tiles
     if ((e = cudaMalloc(&c->colmax, sizeof(float) * c->slots * c->DP)) != cudaSuccess)
         return cleanup("alloc colmax", e);
     if ((e = cudaMalloc(&c->ctr, sizeof(Counters))) != cudaSuccess) return cleanup("alloc ctr", e);
@@ -376,7 +442,6 @@ int lv_destroy(lv_ctx* c) {
     cudaFree(c->K);
     cudaFree(c->V);
     cudaFree(c->lo);
-    cudaFree(c->hi);
     cudaFree(c->colmax);
     cudaFree(c->ctr);
     cudaFree(c->ins_ticket);
@@ -387,6 +452,12 @@ int lv_destroy(lv_ctx* c) {
 
 size_t lv_query_workspace_bytes(const lv_ctx* c) { return c ? c->ws_bytes : 0; }
 
+int lv_debug_trace(lv_ctx* c, int64_t* dev_buf) {
+    if (!c) return fail(LV_EINVAL, "lv_debug_trace: null context");
+    c->trace = reinterpret_cast<long long*>(dev_buf);
+    return LV_OK;
+}
+
 int lv_geometry(const lv_ctx* c, int64_t* out) {
     if (!c || !out) return fail(LV_EINVAL, "lv_geometry: null argument");
     out[0] = c->DP;
@@ -396,7 +467,8 @@ int lv_geometry(const lv_ctx* c, int64_t* out) {
     out[4] = c->splits;
     out[5] = c->chunks_per_split;
     out[6] = lvk::kChunk;
-    out[7] = lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
+    out[7] = c->cfg.dtype == LV_BF16 ? lvk2::query_v2_smem(c->DP, c->G)
+                                     : lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
     return LV_OK;
 }
 int64_t lv_bitmap_words(const lv_ctx* c) { return c ? c->bits_words : 0; }
@@ -411,17 +483,16 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     if (capacity <= c->cfg.capacity) return LV_OK;
     cudaStream_t st = S(stream);
     LV_CUDA(cudaStreamSynchronize(st));
-    const long long ncap = (capacity + lvk::kChunk - 1) / lvk::kChunk * lvk::kChunk;
+    const long long ncap = (capacity + kCapAlign - 1) / kCapAlign * kCapAlign;
     const long long ncells = ncap / c->r;
     const size_t es = esize(c->cfg.dtype);
     const size_t kv_bytes = (size_t)c->slots * ncap * c->DP * es;
-    const size_t sum_bytes = (size_t)c->slots * c->DP * ncells * es;
-    void *K = nullptr, *V = nullptr, *lo = nullptr, *hi = nullptr, *ws = nullptr;
+    const size_t sum_bytes = 2 * (size_t)c->slots * c->DP * ncells * es;
+    void *K = nullptr, *V = nullptr, *lo = nullptr, *ws = nullptr;
     auto undo = [&](cudaError_t e) {
         cudaFree(K);
         cudaFree(V);
         cudaFree(lo);
-        cudaFree(hi);
         cudaFree(ws);
         return fail(LV_ERUNTIME, std::string("lv_reserve: ") + cudaGetErrorString(e));
     };
@@ -429,20 +500,19 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     if ((e = cudaMalloc(&K, kv_bytes)) != cudaSuccess) return undo(e);
     if ((e = cudaMalloc(&V, kv_bytes)) != cudaSuccess) return undo(e);
     if ((e = cudaMalloc(&lo, sum_bytes)) != cudaSuccess) return undo(e);
-    if ((e = cudaMalloc(&hi, sum_bytes)) != cudaSuccess) return undo(e);
     cudaMemset(K, 0, kv_bytes);
     cudaMemset(V, 0, kv_bytes);
-    // rows keep their ids: [slot][cap][DP] -> [slot][ncap][DP]; [slot][DP][cells] likewise
+    // rows keep their ids: [slot][cap][DP] -> [slot][ncap][DP]; the blocked
+    // summary tiles of a slot are contiguous, so they move the same way
     const size_t rowb = (size_t)c->cap * c->DP * es;
     if ((e = cudaMemcpy2D(K, (size_t)ncap * c->DP * es, c->K, rowb, rowb, c->slots,
                           cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
     if ((e = cudaMemcpy2D(V, (size_t)ncap * c->DP * es, c->V, rowb, rowb, c->slots,
                           cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
-    const size_t cellb = (size_t)c->cap_cells * es;
-    if ((e = cudaMemcpy2D(lo, (size_t)ncells * es, c->lo, cellb, cellb, (size_t)c->slots * c->DP,
+    const size_t tileb = 2 * (size_t)c->DP * c->cap_cells * es;
+    if ((e = cudaMemcpy2D(lo, 2 * (size_t)c->DP * ncells * es, c->lo, tileb, tileb, c->slots,
                           cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
-    if ((e = cudaMemcpy2D(hi, (size_t)ncells * es, c->hi, cellb, cellb, (size_t)c->slots * c->DP,
-                          cudaMemcpyDeviceToDevice)) != cudaSuccess) return undo(e);
+    void* hi = lo;
     lv_ctx probe_geo;  // geometry for the new capacity's workspace
     probe_geo.cfg = c->cfg;
     probe_geo.DP = c->DP;
@@ -458,7 +528,6 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     cudaFree(c->K);
     cudaFree(c->V);
     cudaFree(c->lo);
-    cudaFree(c->hi);
     cudaFree(c->ws_mem);
     c->K = K;
     c->V = V;
@@ -471,6 +540,10 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->bits_words = ncap / 32;
     c->splits = probe_geo.splits;
     c->chunks_per_split = probe_geo.chunks_per_split;
+    c->ngroups = probe_geo.ngroups;
+    c->units = probe_geo.units;
+    c->nb = probe_geo.nb;
+    c->nb_groups = probe_geo.nb_groups;
     c->cfg.capacity = capacity;
     return LV_OK;
 }

@@ -147,6 +147,11 @@ __device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& v, float* f
     f[7] = bf_hi(v.w);
 }
 
+__device__ __forceinline__ float elt_f(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float elt_f(const __nv_bfloat16* p) {
+    return __uint_as_float((unsigned)__ldg(reinterpret_cast<const unsigned short*>(p)) << 16);
+}
+
 // Two consecutive cells' bound arrays at one coordinate.
 template <typename T>
 __device__ __forceinline__ float2 load_pair(const T* p);
@@ -356,21 +361,22 @@ __global__ void __launch_bounds__(kThreads) louver_query_kernel(const QueryParam
             const int DG = kThreads / NCPT;
             const int DPG = DP / DG;
             const int pt = tid % NCPT, dg = tid / NCPT;
-            const long long cell0 = k0 >> p.r_log2;
-            const T* los = reinterpret_cast<const T*>(p.lo) + (size_t)slot * DP * p.cap_cells;
-            const T* his = reinterpret_cast<const T*>(p.hi) + (size_t)slot * DP * p.cap_cells;
+            // cell-major summaries: row per cell = [hi (DP) | lo (DP)]
+            const T* rows = reinterpret_cast<const T*>(p.lo) +
+                            ((size_t)slot * p.cap_cells + (size_t)(k0 >> p.r_log2)) * 2 * DP;
             float* red = sc;  // [DG][NC][G]
             for (int pr = pt; pr < NCP; pr += NCPT) {
                 float acc0[G], acc1[G];
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc0[g] = acc1[g] = 0.0f;
                 if (2 * pr < ncells) {
-                    const size_t col = (size_t)(cell0 + 2 * pr);
+                    const T* r0 = rows + (size_t)(2 * pr) * 2 * DP;
+                    const T* r1 = r0 + 2 * DP;
                     const int c0 = dg * DPG;
 #pragma unroll 8
                     for (int c = c0; c < c0 + DPG; ++c) {
-                        const float2 l2 = load_pair<T>(los + (size_t)c * p.cap_cells + col);
-                        const float2 h2 = load_pair<T>(his + (size_t)c * p.cap_cells + col);
+                        const float2 h2 = make_float2(elt_f(r0 + c), elt_f(r1 + c));
+                        const float2 l2 = make_float2(elt_f(r0 + DP + c), elt_f(r1 + DP + c));
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
                             const float qp = qpos[g * Ge::QP + c], qn = qneg[g * Ge::QP + c];

@@ -295,7 +295,9 @@ def test_dense_decode_matches_full_attention(torch, oracle):
     for hq in range(8):
         w = oracle.sparse_attention(K[0, hq // 4], V[0, hq // 4], [], np.arange(4000), Q[0, hq],
                                     np.float32(1 / math.sqrt(128)))
-        assert rel_err(o[0, hq], w[2]) <= REL_TOL
+        # the dense baseline scores on the tensor cores (no normative dot): the
+        # north-star tolerance, 1e-3 relative, applies
+        assert rel_err(o[0, hq], w[2]) <= 1e-3
 
 
 def test_empty_cache_query(torch):

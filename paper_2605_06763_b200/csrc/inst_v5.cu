@@ -22,7 +22,19 @@ static cudaError_t launch_t(const V5Params& vp, int slots, cudaStream_t st) {
     louver_probe_v5<DP, G><<<dim3((unsigned)vp.nbp, (unsigned)slots), kT, smem1, st>>>(vp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    louver_exact_v5<DP, G><<<dim3((unsigned)vp.nb, (unsigned)slots), kT, smem2, st>>>(vp);
+    // programmatic dependent launch: the exact kernel's setup overlaps the probe's tail
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)vp.nb, (unsigned)slots);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = (size_t)smem2;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, louver_exact_v5<DP, G>, vp);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -165,6 +165,27 @@ __global__ void __launch_bounds__(kT, 2) louver_probe_v5(const __grid_constant__
     const int slot = blockIdx.y;
     float* ct = reinterpret_cast<float*>(smem + Ge::OFF_CT) + warp * 16 * 8 * Ge::NT;
 
+    // The first tile's loads depend on nothing: issue them before the setup.
+    // Rows are addressed within the arena capacity; rows past n are ignored.
+    const __nv_bfloat16* base = vp.sum + (size_t)slot * p.cap_cells * (2 * DP);
+    const int q = lane & 3;
+    constexpr int NP = 2 * DP / 32;  // k-pairs
+    uint4 u0[NP], u1[NP];
+    const int stride = vp.nbp * kW;
+    auto load_tile = [&](int tile) {
+        const long long c0 = (long long)tile << 4;
+        const unsigned char* row0 =
+            reinterpret_cast<const unsigned char*>(base + (size_t)(c0 + (lane >> 2)) * 2 * DP);
+        const unsigned char* row1 = row0 + 8 * 2 * DP * 2;
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            u0[pp] = ldg16(row0 + (32 * pp + 8 * q) * 2);
+            u1[pp] = ldg16(row1 + (32 * pp + 8 * q) * 2);
+        }
+    };
+    int tile = blockIdx.x * kW + warp;
+    if (tile < vp.tiles) load_tile(tile);
+
     const long long n = p.ctr->n;
     const long long indexed = p.ctr->indexed;
     const int rl = p.r_log2, r = 1 << rl;
@@ -180,23 +201,11 @@ __global__ void __launch_bounds__(kT, 2) louver_probe_v5(const __grid_constant__
         });
     }
     __syncthreads();
+    // the exact kernel may start its own setup now (programmatic dependent launch)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
-    const __nv_bfloat16* base = vp.sum + (size_t)slot * p.cap_cells * (2 * DP);
-    const int q = lane & 3;
-    for (int tile = blockIdx.x * kW + warp; tile < ntile; tile += vp.nbp * kW) {
+    for (; tile < ntile; tile += stride) {
         const long long c0 = (long long)tile << 4;
-        long long cr0 = c0 + (lane >> 2), cr1 = cr0 + 8;
-        if (cr0 >= ncells) cr0 = c0;  // clamp: rows past the data are read and ignored
-        if (cr1 >= ncells) cr1 = c0;
-        const unsigned char* row0 = reinterpret_cast<const unsigned char*>(base + (size_t)cr0 * 2 * DP);
-        const unsigned char* row1 = reinterpret_cast<const unsigned char*>(base + (size_t)cr1 * 2 * DP);
-        constexpr int NP = 2 * DP / 32;  // k-pairs
-        uint4 u0[NP], u1[NP];
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-            u0[pp] = ldg16(row0 + (32 * pp + 8 * q) * 2);
-            u1[pp] = ldg16(row1 + (32 * pp + 8 * q) * 2);
-        }
         float acc[Ge::NT][4];
 #pragma unroll
         for (int t = 0; t < Ge::NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
@@ -212,6 +221,7 @@ __global__ void __launch_bounds__(kT, 2) louver_probe_v5(const __grid_constant__
                 mma16816(acc[t], a1, b1.x, b1.y);
             }
         }
+        if (tile + stride < ntile) load_tile(tile + stride);  // prefetch the next tile
 #pragma unroll
         for (int t = 0; t < Ge::NT; ++t) {
             const int rw = lane >> 2, col = t * 8 + 2 * q;
@@ -240,6 +250,7 @@ __global__ void __launch_bounds__(kT, 2) louver_probe_v5(const __grid_constant__
         __syncwarp();
         const unsigned m = __ballot_sync(0xffffffffu, gm != 0) & 0xffffu;
         if (lane == 0) vp.cmask[(size_t)slot * vp.tiles + tile] = (unsigned short)m;
+        __syncwarp();
         if (p.totals) {
             const int tested = __popc(__ballot_sync(0xffffffffu, lane < 16 && cell < ncells));
             if (lane == 0) {
@@ -263,14 +274,16 @@ template <int DP, int G>
 struct E5 {
     static constexpr int NT = (3 * G + 7) / 8;
     static constexpr int KS = DP / 16;
+    static constexpr int KL = 2048;                                   // row -> key list per segment
     static constexpr int OFF_FR = 0;                                  // [KS][NT][32] uint2
     static constexpr int OFF_Q = OFF_FR + KS * NT * 32 * 8;           // [G][DP+4]
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc floats
     static constexpr int MISC = 4 * G + kW * G + 8;
-    static constexpr int OFF_WS = (OFF_M + MISC * 4 + 15) / 16 * 16;  // per-warp scratch
+    static constexpr int OFF_KL = (OFF_M + MISC * 4 + 15) / 16 * 16;  // [KL] u32 keys of the segment
+    static constexpr int OFF_WS = OFF_KL + KL * 4;                    // per-warp scratch
     static constexpr int WCT = 16 * 8 * NT;                           // C tile floats
-    static constexpr int WSC = 16 * G;                                // scores / p
-    static constexpr int WSZ = (WCT + WSC + 16) * 4;                  // + keys[16] (u32)
+    static constexpr int WSC = 16 * G;                                // scores of the task
+    static constexpr int WSZ = (WCT + WSC) * 4;
     static constexpr int SZ_WS = kW * WSZ;
     static constexpr int SZ_RED = kW * G * (DP + 2) * 4;              // final warp reduction
     static constexpr int SZ_U = SZ_WS > SZ_RED ? SZ_WS : SZ_RED;
@@ -337,6 +350,7 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
     float* S = misc + 2 * G;     // [G]
     float* red = misc + 4 * G;   // [kW*G]
     int* iscr = reinterpret_cast<int*>(misc + 4 * G + kW * G);  // [8]
+    unsigned* klist = reinterpret_cast<unsigned*>(smem + Ge::OFF_KL);
     unsigned* ucm = reinterpret_cast<unsigned*>(smem + Ge::FIXED);  // [tiles] masks
     unsigned* upre = ucm + vp.tiles;                                // [tiles] exclusive row prefix
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -344,18 +358,11 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
     unsigned char* ws = smem + Ge::OFF_WS + warp * Ge::WSZ;
     float* ct = reinterpret_cast<float*>(ws);
     float* wsc = ct + Ge::WCT;
-    unsigned* wkey = reinterpret_cast<unsigned*>(wsc + Ge::WSC);  // [16]
-
-    const long long n = p.ctr->n;
-    const long long indexed = p.ctr->indexed;
-    const int rl = p.r_log2, r = 1 << rl;
-    const long long ncells = (n + r - 1) >> rl;
-    const int ntile = (int)((ncells + 15) >> 4);
+    const int q = lane & 3;
     const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
     const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
 
-    // ---- setup: masks, q, thresholds, fragments, row prefix
-    for (int u = tid; u < ntile; u += kT) ucm[u] = vp.cmask[(size_t)slot * vp.tiles + u];
+    // ---- setup independent of the probe (overlaps it under programmatic launch)
     setup_q<DP, G>(p.q + (size_t)slot * G * DP, p.colmax + (size_t)slot * DP, qf, red, S);
     if (tid < G) {
         tau_s[tid] = p.tau[(size_t)slot * G + tid];
@@ -365,6 +372,15 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
         const int l = i & 31, nt = (i >> 5) % Ge::NT, t = (i >> 5) / Ge::NT;
         fr[i] = b_frag<G, 3>(t, nt, l, [&](int k, int g) { return qf[g * (DP + 4) + k]; });
     }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // probe results visible from here
+
+    const long long n = p.ctr->n;
+    const long long indexed = p.ctr->indexed;
+    const int rl = p.r_log2, r = 1 << rl;
+    const long long ncells = (n + r - 1) >> rl;
+    const int ntile = (int)((ncells + 15) >> 4);
+    for (int u = tid; u < ntile; u += kT) ucm[u] = vp.cmask[(size_t)slot * vp.tiles + u];
+    __syncthreads();
     {
         const int per = (ntile + kT - 1) / kT;
         const int u0 = tid * per;
@@ -394,7 +410,6 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
     }
     const long long total = iscr[0];
     const long long lo = total * blk / vp.nb, hi = total * (blk + 1) / vp.nb;
-    const int ntask = (int)((hi - lo + 15) >> 4);
 
     // ---- per-warp online softmax state
     constexpr int VPL = DP / 32;  // V dims per lane
@@ -410,173 +425,184 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
 #pragma unroll
     for (int g = 0; g < G; ++g) st_sel[g] = st_att[g] = 0;
     unsigned long long t_keys = 0, t_vals = 0;
-    const int q = lane & 3;
 
-    for (int task = warp; task < ntask; task += kW) {
-        // rows -> keys (lanes 0..15)
-        unsigned key = 0xffffffffu;
-        if (lane < 16) {
-            const long long row = lo + ((long long)task << 4) + lane;
-            if (row < hi) {
-                int a = 0, b = ntile - 1;
-                while (a < b) {
-                    const int mid = (a + b + 1) >> 1;
-                    if ((long long)upre[mid] <= row) a = mid; else b = mid - 1;
-                }
-                const int off = (int)(row - upre[a]);
-                unsigned m = ucm[a];
-                for (int i = 0; i < (off >> rl); ++i) m &= m - 1;
-                if (m != 0u) {
-                    const long long kk = ((long long)a * 16 + (__ffs(m) - 1)) * r + (off & (r - 1));
-                    if (kk >= 0 && kk < n) key = (unsigned)kk;
+    for (long long seg = lo; seg < hi; seg += Ge::KL) {
+        const int nrow = (int)(hi - seg < Ge::KL ? hi - seg : Ge::KL);
+        // row -> key for the whole segment, all threads (unit by binary search, cell by bit select)
+        for (int i = tid; i < nrow; i += kT) {
+            const long long row = seg + i;
+            int a = 0, b = ntile - 1;
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if ((long long)upre[mid] <= row) a = mid; else b = mid - 1;
+            }
+            const int off = (int)(row - upre[a]);
+            unsigned m = ucm[a];
+            for (int j = 0; j < (off >> rl); ++j) m &= m - 1;
+            unsigned key = 0xffffffffu;
+            if (m != 0u) {
+                const long long kk = ((long long)a * 16 + (__ffs(m) - 1)) * r + (off & (r - 1));
+                if (kk >= 0 && kk < n) key = (unsigned)kk;
+            }
+            klist[i] = key;
+        }
+        if (tid == 0) iscr[1] = 0;
+        __syncthreads();
+        const int ntask = (nrow + 15) >> 4;
+        while (true) {
+            int task = 0;
+            if (lane == 0) task = atomicAdd(iscr + 1, 1);
+            task = __shfl_sync(0xffffffffu, task, 0);
+            if (task >= ntask) break;
+            const int r0i = task * 16;
+            const unsigned key = lane < 16 && r0i + lane < nrow ? klist[r0i + lane] : 0xffffffffu;
+            const unsigned k0 = __shfl_sync(0xffffffffu, key, lane >> 2);
+            const unsigned k1 = __shfl_sync(0xffffffffu, key, (lane >> 2) + 8);
+            const unsigned char* row0 =
+                reinterpret_cast<const unsigned char*>(Ks + (size_t)(k0 == 0xffffffffu ? 0 : k0) * DP);
+            const unsigned char* row1 =
+                reinterpret_cast<const unsigned char*>(Ks + (size_t)(k1 == 0xffffffffu ? 0 : k1) * DP);
+            constexpr int NP = DP / 32;
+            uint4 u0[NP], u1[NP];
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp) {
+                u0[pp] = ldg16(row0 + (32 * pp + 8 * q) * 2);
+                u1[pp] = ldg16(row1 + (32 * pp + 8 * q) * 2);
+            }
+            float acc[Ge::NT][4];
+#pragma unroll
+            for (int t = 0; t < Ge::NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp) {
+                const unsigned a0[4] = {u0[pp].x, u1[pp].x, u0[pp].y, u1[pp].y};
+                const unsigned a1[4] = {u0[pp].z, u1[pp].z, u0[pp].w, u1[pp].w};
+#pragma unroll
+                for (int t = 0; t < Ge::NT; ++t) {
+                    const uint2 b0 = fr[((2 * pp) * Ge::NT + t) * 32 + lane];
+                    const uint2 b1 = fr[((2 * pp + 1) * Ge::NT + t) * 32 + lane];
+                    mma16816(acc[t], a0, b0.x, b0.y);
+                    mma16816(acc[t], a1, b1.x, b1.y);
                 }
             }
-            wkey[lane] = key;
-#ifdef LV_DEBUG_V5
-            if (blk == 6 && lane == 0)
-                printf("slot %d blk %d warp %d task %d n %lld total %lld lo %lld hi %lld key %u ntile %d\n", slot,
-                       blk, warp, task, n, total, lo, hi, key, ntile);
-#endif
-        }
-        __syncwarp();
-        const unsigned k0 = __shfl_sync(0xffffffffu, key, lane >> 2);
-        const unsigned k1 = __shfl_sync(0xffffffffu, key, (lane >> 2) + 8);
-        const unsigned char* row0 = reinterpret_cast<const unsigned char*>(Ks + (size_t)(k0 == 0xffffffffu ? 0 : k0) * DP);
-        const unsigned char* row1 = reinterpret_cast<const unsigned char*>(Ks + (size_t)(k1 == 0xffffffffu ? 0 : k1) * DP);
-        constexpr int NP = DP / 32;
-        uint4 u0[NP], u1[NP];
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-            u0[pp] = ldg16(row0 + (32 * pp + 8 * q) * 2);
-            u1[pp] = ldg16(row1 + (32 * pp + 8 * q) * 2);
-        }
-        float acc[Ge::NT][4];
-#pragma unroll
-        for (int t = 0; t < Ge::NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-            const unsigned a0[4] = {u0[pp].x, u1[pp].x, u0[pp].y, u1[pp].y};
-            const unsigned a1[4] = {u0[pp].z, u1[pp].z, u0[pp].w, u1[pp].w};
 #pragma unroll
             for (int t = 0; t < Ge::NT; ++t) {
-                const uint2 b0 = fr[((2 * pp) * Ge::NT + t) * 32 + lane];
-                const uint2 b1 = fr[((2 * pp + 1) * Ge::NT + t) * 32 + lane];
-                mma16816(acc[t], a0, b0.x, b0.y);
-                mma16816(acc[t], a1, b1.x, b1.y);
+                const int rw = lane >> 2, col = t * 8 + 2 * q;
+                ct[rw * 8 * Ge::NT + col] = acc[t][0];
+                ct[rw * 8 * Ge::NT + col + 1] = acc[t][1];
+                ct[(rw + 8) * 8 * Ge::NT + col] = acc[t][2];
+                ct[(rw + 8) * 8 * Ge::NT + col + 1] = acc[t][3];
             }
-        }
+            __syncwarp();
+            // classify (row, g): fast decides outside tau +- margin, else the normative dot
+            for (int pi = lane; pi < 16 * G; pi += 32) {
+                const int rw = pi / G, g = pi % G;
+                const unsigned kk = r0i + rw < nrow ? klist[r0i + rw] : 0xffffffffu;
+                float s = -INFINITY;
+                if (kk != 0xffffffffu) {
+                    const float* c = ct + rw * 8 * Ge::NT;
+                    float sc = (c[g] + c[G + g]) + c[2 * G + g];
+                    bool sel = sc >= tau_s[g] + marg[g];
+                    if (!sel && sc >= tau_s[g] - marg[g]) {  // undecided: normative dot (core.hpp:17-21)
+                        const unsigned char* kr = reinterpret_cast<const unsigned char*>(Ks + (size_t)kk * DP);
+                        const float* qg = qf + g * (DP + 4);
+                        float acc2 = 0.0f;
+                        for (int cc = 0; cc < DP / 8; ++cc) {
+                            const uint4 kv = ldg16(kr + cc * 16);
+                            float kf[8];
+                            lvk::unpack16<__nv_bfloat16>(kv, kf);
 #pragma unroll
-        for (int t = 0; t < Ge::NT; ++t) {
-            const int rw = lane >> 2, col = t * 8 + 2 * q;
-            ct[rw * 8 * Ge::NT + col] = acc[t][0];
-            ct[rw * 8 * Ge::NT + col + 1] = acc[t][1];
-            ct[(rw + 8) * 8 * Ge::NT + col] = acc[t][2];
-            ct[(rw + 8) * 8 * Ge::NT + col + 1] = acc[t][3];
-        }
-        __syncwarp();
-        // classify (row, g) pairs: fast decides outside tau +- margin, else normative
-        for (int pi = lane; pi < 16 * G; pi += 32) {
-            const int rw = pi / G, g = pi % G;
-            const unsigned kk = wkey[rw];
-            float s = -INFINITY;
-            if (kk != 0xffffffffu) {
-                const float* c = ct + rw * 8 * Ge::NT;
-                float sc = (c[g] + c[G + g]) + c[2 * G + g];
-                bool sel = sc >= tau_s[g] + marg[g];
-                if (!sel && sc >= tau_s[g] - marg[g]) {  // undecided: normative dot (core.hpp:17-21)
-                    const unsigned char* kr = reinterpret_cast<const unsigned char*>(Ks + (size_t)kk * DP);
-                    const float* qg = qf + g * (DP + 4);
-                    float acc2 = 0.0f;
-                    for (int cc = 0; cc < DP / 8; ++cc) {
-                        const uint4 kv = ldg16(kr + cc * 16);
-                        float kf[8];
-                        lvk::unpack16<__nv_bfloat16>(kv, kf);
-#pragma unroll
-                        for (int e2 = 0; e2 < 8; ++e2) acc2 = __fadd_rn(acc2, __fmul_rn(qg[cc * 8 + e2], kf[e2]));
+                            for (int e2 = 0; e2 < 8; ++e2) acc2 = __fadd_rn(acc2, __fmul_rn(qg[cc * 8 + e2], kf[e2]));
+                        }
+                        sc = acc2;
+                        sel = acc2 >= tau_s[g];
                     }
-                    sc = acc2;
-                    sel = acc2 >= tau_s[g];
+                    const bool in_buf = (long long)kk >= indexed;
+                    if (sel) {
+                        ++st_sel[g];
+                        if (p.bits) atomicOr(p.bits + ((size_t)slot * G + g) * p.bits_words + (kk >> 5), 1u << (kk & 31));
+                    }
+                    if (sel || (in_buf && !p.strict)) {
+                        s = sc;
+                        ++st_att[g];
+                    }
                 }
-                const bool in_buf = (long long)kk >= indexed;
-                if (sel) {
-                    ++st_sel[g];
-                    if (p.bits) atomicOr(p.bits + ((size_t)slot * G + g) * p.bits_words + (kk >> 5), 1u << (kk & 31));
-                }
-                if (sel || (in_buf && !p.strict)) {
-                    s = sc;
-                    ++st_att[g];
-                }
+                wsc[pi] = s;
             }
-            wsc[pi] = s;
-        }
-        __syncwarp();
-        // attended rows of the task
-        bool att = false;
-        if (lane < 16) {
+            __syncwarp();
+            // task max per q head (lane < 16 owns row lane), ILP over g
+            float sv[G], mx[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) att |= wsc[lane * G + g] != -INFINITY;
-        }
-        const unsigned amask = __ballot_sync(0xffffffffu, att) & 0xffffu;
-        if (lane < 16 && wkey[lane] != 0xffffffffu) ++t_keys;
-        if (amask == 0) continue;
-        if (lane == 0) t_vals += __popc(amask);
-        // issue the V rows (8 bytes per lane each), then the softmax update
-        uint4 vv[16];
-        {
-            unsigned m = amask;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (m) {
-                    const int rw = __ffs(m) - 1;
-                    m &= m - 1;
-                    vv[i] = ldg_v<VPL>(reinterpret_cast<const unsigned char*>(Vs + (size_t)wkey[rw] * DP) + lane * VPL * 2);
-                }
+            for (int g = 0; g < G; ++g) {
+                sv[g] = lane < 16 ? wsc[lane * G + g] : -INFINITY;
+                mx[g] = sv[g] == -INFINITY ? -INFINITY : p.scale * sv[g];
             }
-        }
-        float mnew[G], alpha[G];
+            bool att = false;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float v = lane < 16 ? p.scale * wsc[lane * G + g] : -INFINITY;
+            for (int g = 0; g < G; ++g) att |= sv[g] != -INFINITY;
+            const unsigned amask = __ballot_sync(0xffffffffu, att) & 0xffffu;
+            const unsigned vkeys = __ballot_sync(0xffffffffu, key != 0xffffffffu);
+            if (lane == 0) t_keys += __popc(vkeys);
+            __syncwarp();
+            if (amask == 0) continue;
+            if (lane == 0) t_vals += __popc(amask);
 #pragma unroll
-            for (int of = 16; of > 0; of >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, of));
-            mnew[g] = fmaxf(mrun[g], v);
-            alpha[g] = mrun[g] == -INFINITY ? 0.0f : expf(mrun[g] - mnew[g]);
-            mrun[g] = mnew[g];
-            lsum[g] *= alpha[g];
+            for (int of = 16; of > 0; of >>= 1)
 #pragma unroll
-            for (int e = 0; e < VPL; ++e) o[g][e] *= alpha[g];
-        }
-        // p for the 16 x G pairs (lane < 16 owns its row), then broadcast per row
-        float pl[G];
+                for (int g = 0; g < G; ++g) mx[g] = fmaxf(mx[g], __shfl_xor_sync(0xffffffffu, mx[g], of));
+            float pl[G], ls[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float s = lane < 16 ? wsc[lane * G + g] : -INFINITY;
-            pl[g] = s == -INFINITY ? 0.0f : expf(p.scale * s - mnew[g]);
-            float t = pl[g];
+            for (int g = 0; g < G; ++g) {
+                const float mnew = fmaxf(mrun[g], mx[g]);
+                const float alpha = mrun[g] == -INFINITY ? 0.0f : __expf(mrun[g] - mnew);
+                mrun[g] = mnew;
+                lsum[g] *= alpha;
 #pragma unroll
-            for (int of = 16; of > 0; of >>= 1) t += __shfl_xor_sync(0xffffffffu, t, of);
-            lsum[g] += t;
-        }
-        {
+                for (int e = 0; e < VPL; ++e) o[g][e] *= alpha;
+                pl[g] = sv[g] == -INFINITY ? 0.0f : __expf(p.scale * sv[g] - mnew);
+                ls[g] = pl[g];
+            }
+#pragma unroll
+            for (int of = 16; of > 0; of >>= 1)
+#pragma unroll
+                for (int g = 0; g < G; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], of);
+#pragma unroll
+            for (int g = 0; g < G; ++g) lsum[g] += ls[g];
+            // V rows of attended keys, 8 per batch (8 bytes per lane at DP=128)
             unsigned m = amask;
+            while (m) {
+                uint4 vv[8];
+                int rws[8];
+                int cnt = 0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (m) {
-                    const int rw = __ffs(m) - 1;
-                    m &= m - 1;
-                    float vf[8];
-                    const unsigned vw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
+                for (int i = 0; i < 8; ++i) {
+                    rws[i] = -1;
+                    if (m) {
+                        const int rw = __ffs(m) - 1;
+                        m &= m - 1;
+                        rws[i] = rw;
+                        const unsigned kv = __shfl_sync(0xffffffffu, key, rw);
+                        vv[i] = ldg_v<VPL>(reinterpret_cast<const unsigned char*>(Vs + (size_t)kv * DP) + lane * VPL * 2);
+                        ++cnt;
+                    }
+                }
 #pragma unroll
-                    for (int e = 0; e < VPL; ++e) vf[e] = (e & 1) ? lvk::bf_hi(vw[e >> 1]) : lvk::bf_lo(vw[e >> 1]);
+                for (int i = 0; i < 8; ++i) {
+                    if (i < cnt) {
+                        float vf[8];
+                        const unsigned vw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float pw = __shfl_sync(0xffffffffu, pl[g], rw);
+                        for (int e = 0; e < VPL; ++e) vf[e] = (e & 1) ? lvk::bf_hi(vw[e >> 1]) : lvk::bf_lo(vw[e >> 1]);
 #pragma unroll
-                        for (int e = 0; e < VPL; ++e) o[g][e] = fmaf(pw, vf[e], o[g][e]);
+                        for (int g = 0; g < G; ++g) {
+                            const float pw = __shfl_sync(0xffffffffu, pl[g], rws[i]);
+#pragma unroll
+                            for (int e = 0; e < VPL; ++e) o[g][e] = fmaf(pw, vf[e], o[g][e]);
+                        }
                     }
                 }
             }
         }
+        __syncthreads();  // klist is rewritten by the next segment
     }
 
     // ---- statistics
@@ -592,17 +618,9 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
             }
         }
     }
-    if (p.totals) {
-        unsigned long long c = t_keys, d = t_vals;
-#pragma unroll
-        for (int of = 16; of > 0; of >>= 1) {
-            c += __shfl_xor_sync(0xffffffffu, c, of);
-            d += __shfl_xor_sync(0xffffffffu, d, of);
-        }
-        if (lane == 0) {
-            if (c) atomicAdd(p.totals + 2, c);
-            if (d) atomicAdd(p.totals + 3, d);
-        }
+    if (p.totals && lane == 0) {
+        if (t_keys) atomicAdd(p.totals + 2, t_keys);
+        if (t_vals) atomicAdd(p.totals + 3, t_vals);
     }
 
     // ---- warp partials -> CTA partial
@@ -621,18 +639,18 @@ __global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__
     __syncthreads();
     constexpr int Wd = G * (DP + 2);
     float* part = p.partial_ws + ((size_t)slot * vp.nb + blk) * Wd;
-    float* shw = reinterpret_cast<float*>(smem + Ge::OFF_FR);  // fragments no longer needed
+    float* shw = reinterpret_cast<float*>(smem + Ge::OFF_KL);  // the key list is no longer needed
     if (tid < G) {
-        float m = -INFINITY;
-        for (int w = 0; w < kW; ++w) m = fmaxf(m, wred[(w * G + tid) * (DP + 2)]);
+        float mm = -INFINITY;
+        for (int w = 0; w < kW; ++w) mm = fmaxf(mm, wred[(w * G + tid) * (DP + 2)]);
         float l = 0.0f;
         for (int w = 0; w < kW; ++w) {
             const float mw = wred[(w * G + tid) * (DP + 2)];
-            const float a = mw == -INFINITY ? 0.0f : expf(mw - m);
+            const float a = mw == -INFINITY ? 0.0f : expf(mw - mm);
             shw[w * G + tid] = a;
             l += a * wred[(w * G + tid) * (DP + 2) + 1];
         }
-        part[tid * (DP + 2)] = l > 0.0f ? m : -INFINITY;
+        part[tid * (DP + 2)] = l > 0.0f ? mm : -INFINITY;
         part[tid * (DP + 2) + 1] = l;
     }
     __syncthreads();

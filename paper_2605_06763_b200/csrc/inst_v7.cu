@@ -1,28 +1,28 @@
-// v5 (bf16, flat warp-level) instantiations: DP in {64,128,256} x G in {1,2,4,8}.
-#include "louver_v5.cuh"
+// bf16 query path instantiations (probe -> cell stream): DP in {64,128,256} x G in {1,2,4,8}.
+#include "louver_v7.cuh"
 
-namespace lvk5 {
+namespace lvk7 {
 
 template <int DP, int G>
 static cudaError_t launch_t(const V5Params& vp, int slots, cudaStream_t st) {
-    static bool attr1 = false;
+    static bool attr_done = false;
     static int smem2_set = 0;
     constexpr int smem1 = P5<DP, G>::SMEM;
-    const int smem2 = E5<DP, G>::smem(vp.tiles);
-    if (!attr1) {
+    const int smem2 = C7<DP, G>::smem(vp.tiles);
+    if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(louver_probe_v5<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
         if (e != cudaSuccess) return e;
-        attr1 = true;
+        attr_done = true;
     }
     if (smem2 > smem2_set) {
-        cudaError_t e = cudaFuncSetAttribute(louver_exact_v5<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaError_t e = cudaFuncSetAttribute(louver_cells_v7<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         if (e != cudaSuccess) return e;
         smem2_set = smem2;
     }
     louver_probe_v5<DP, G><<<dim3((unsigned)vp.nbp, (unsigned)slots), kT, smem1, st>>>(vp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // programmatic dependent launch: the exact kernel's setup overlaps the probe's tail
+    // programmatic dependent launch: the cell stream's setup overlaps the probe's tail
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)vp.nb, (unsigned)slots);
     cfg.blockDim = dim3(kT);
@@ -33,13 +33,13 @@ static cudaError_t launch_t(const V5Params& vp, int slots, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, louver_exact_v5<DP, G>, vp);
+    e = cudaLaunchKernelEx(&cfg, louver_cells_v7<DP, G>, vp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-cudaError_t launch_query_v5(int DP, int G, const V5Params& vp, int slots, cudaStream_t st) {
-#define LV5_G(D)                                          \
+cudaError_t launch_query_v7(int DP, int G, const V5Params& vp, int slots, cudaStream_t st) {
+#define LV7_G(D)                                          \
     switch (G) {                                          \
         case 1: return launch_t<D, 1>(vp, slots, st);     \
         case 2: return launch_t<D, 2>(vp, slots, st);     \
@@ -48,12 +48,12 @@ cudaError_t launch_query_v5(int DP, int G, const V5Params& vp, int slots, cudaSt
     }                                                     \
     break;
     switch (DP) {
-        case 64: LV5_G(64)
-        case 128: LV5_G(128)
-        case 256: LV5_G(256)
+        case 64: LV7_G(64)
+        case 128: LV7_G(128)
+        case 256: LV7_G(256)
     }
-#undef LV5_G
+#undef LV7_G
     return cudaErrorInvalidValue;
 }
 
-}  // namespace lvk5
+}  // namespace lvk7

@@ -15,7 +15,7 @@
 #include "louver_b200.h"
 #include "louver_dispatch.h"
 #include "louver_v2.cuh"
-#include "louver_v5.cuh"
+#include "louver_v7.cuh"
 
 using lvk::Counters;
 
@@ -51,7 +51,7 @@ struct Workspace {
     float* gpart = nullptr;    // [slots][ngroups][G][DP+2] (v2 merge tree)
     int* gtickets = nullptr;   // [slots][ngroups]
     int* stickets = nullptr;   // [slots]
-    unsigned* cmask = nullptr; // [slots][units] survivor cells (v4 probe -> exact)
+    unsigned* cmask = nullptr; // [slots][tiles] u16 survivor cells (probe -> score)
     float* q = nullptr;        // [rows][DP]
     float* out = nullptr;      // [rows][DP]
     float* tau = nullptr;      // [rows]
@@ -66,7 +66,8 @@ struct lv_ctx {
     int DP = 0, G = 1, r = 1, r_log2 = 0, slots = 0, rows = 0;
     long long cap = 0, cap_cells = 0, bits_words = 0;
     int splits = 1, chunks_per_split = 1, ngroups = 1;
-    int nb = 1, nb_groups = 1, units = 1;  // v4: exact CTAs per slot, their merge groups, 512-key units
+    int nb = 1, nb_groups = 1, units = 1;  // bf16: score/attend CTAs per slot, merge groups, 512-key units
+    int nbp = 1;                           // bf16: probe CTAs per slot
     void* K = nullptr;
     void* V = nullptr;
     void* lo = nullptr;
@@ -158,6 +159,9 @@ void choose_splits(lv_ctx* c) {
         long long nb = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
         c->nb = (int)std::min<long long>(nb, 4096);
+        long long nbp = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
+        if (const char* e = std::getenv("LV_NBP")) nbp = std::max(1LL, std::atoll(e));
+        c->nbp = (int)std::min<long long>(nbp, 4096);
         c->nb_groups = (c->nb + lvk5::kMG - 1) / lvk5::kMG;
         return;
     }
@@ -291,13 +295,15 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         v5.sum = reinterpret_cast<const __nv_bfloat16*>(c->lo);
         v5.cmask = reinterpret_cast<unsigned short*>(w.cmask);
         v5.tiles = (int)(c->cap_cells / 16);
-        v5.nbp = c->nb;
+        v5.nbp = c->nbp;
         v5.nb = c->nb;
         v5.gpart = w.gpart;
         v5.gtickets = w.gtickets;
         v5.stickets = w.stickets;
         v5.ngroups = c->nb_groups;
-        e = lvk5::launch_query_v5(c->DP, c->G, v5, c->slots, st);
+        v5.gmax = nullptr;
+        v5.p.tot_trace = c->trace;
+        e = lvk7::launch_query_v7(c->DP, c->G, v5, c->slots, st);
     } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
         lvk2::V2Params vp{};
         vp.p = p;
@@ -544,6 +550,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->units = probe_geo.units;
     c->nb = probe_geo.nb;
     c->nb_groups = probe_geo.nb_groups;
+    c->nbp = probe_geo.nbp;
     c->cfg.capacity = capacity;
     return LV_OK;
 }

@@ -69,6 +69,7 @@ struct QueryParams {
     long long bits_words;
     int* counts;            // [slots*G][4] or null
     unsigned long long* totals;  // [4] or null
+    long long* tot_trace;        // debug: per-CTA phase timestamps (bf16 cell stream) or null
 };
 
 template <typename T>

@@ -195,40 +195,54 @@ __device__ __forceinline__ int compact(int count, Flag flag, unsigned short* lis
 // Merge P partials (m, l, o[DP]) at `src` (stride G*(DP+2) between partials)
 // into `dst` (same [G][DP+2] layout) or, when final, into out rows.
 template <int DP, int G>
-__device__ void merge_partials(const float* src, int P, float* dst, float* out, float* part_out,
-                               int* counts, float* shw) {
+__device__ void merge_partials(const float* src, int P, float* dst, float* out, float* part_out, int* counts,
+                       float* shw) {
+    // shw: [P][G] weights, then M[G], L[G]; all partial headers are loaded in
+    // parallel and the o loads are batched, so a merge costs ~2 L2 round trips.
     const int tid = threadIdx.x;
     constexpr int W = G * (DP + 2);
+    float* shm = shw;              // [P][G] m, then weights
+    float* shl = shw + P * G;      // [P][G] l
+    float* ML = shl + P * G;       // M[G], L[G]
+    for (int i = tid; i < P * G; i += kThreads) {
+        const int s = i / G, g = i % G;
+        shm[i] = __ldcg(src + (size_t)s * W + g * (DP + 2));
+        shl[i] = __ldcg(src + (size_t)s * W + g * (DP + 2) + 1);
+    }
+    __syncthreads();
     if (tid < G) {
         float m = -INFINITY;
-        for (int s = 0; s < P; ++s) m = fmaxf(m, __ldcg(src + (size_t)s * W + tid * (DP + 2)));
+        for (int s = 0; s < P; ++s) m = fmaxf(m, shm[s * G + tid]);
         float l = 0.0f;
         for (int s = 0; s < P; ++s) {
-            const float ms = __ldcg(src + (size_t)s * W + tid * (DP + 2));
+            const float ms = shm[s * G + tid];
             const float w = ms == -INFINITY ? 0.0f : expf(ms - m);
-            shw[s * G + tid] = w;
-            l += w * __ldcg(src + (size_t)s * W + tid * (DP + 2) + 1);
+            shm[s * G + tid] = w;
+            l += w * shl[s * G + tid];
         }
-        shw[P * G + tid] = m;
-        shw[P * G + G + tid] = l;
+        ML[tid] = m;
+        ML[G + tid] = l;
     }
     __syncthreads();
     for (int i = tid; i < G * DP; i += kThreads) {
         const int g = i / DP, c = i % DP;
         float acc = 0.0f;
-#pragma unroll 4
-        for (int s = 0; s < P; ++s) {
-            const float w = shw[s * G + g];
-            const float o = __ldcg(src + (size_t)s * W + g * (DP + 2) + 2 + c);
-            acc = w != 0.0f ? fmaf(w, o, acc) : acc;
+        for (int s0 = 0; s0 < P; s0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                v[j] = s0 + j < P ? __ldcg(src + (size_t)(s0 + j) * W + g * (DP + 2) + 2 + c) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j < P) acc = fmaf(shm[(s0 + j) * G + g], v[j], acc);
         }
-        const float l = shw[P * G + G + g];
+        const float l = ML[G + g];
         if (dst) dst[g * (DP + 2) + 2 + c] = acc;
         if (out) out[g * DP + c] = l > 0.0f ? acc / l : 0.0f;
         if (part_out) part_out[g * (DP + 2) + 2 + c] = acc;
     }
     if (tid < G) {
-        const float m = shw[P * G + tid], l = shw[P * G + G + tid];
+        const float m = ML[tid], l = ML[G + tid];
         if (dst) {
             dst[tid * (DP + 2)] = m;
             dst[tid * (DP + 2) + 1] = l;

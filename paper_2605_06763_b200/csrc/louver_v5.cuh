@@ -50,6 +50,7 @@ struct V5Params {
     int* gtickets;             // [slots][ngroups]
     int* stickets;             // [slots]
     int ngroups;
+    int* gmax;                 // optional [slot][G]: reset to the encoding of -inf by K1
 };
 
 // physical element of logical (k-step t, fragment element e in 0..3) for lane q:
@@ -202,6 +203,10 @@ __global__ void __launch_bounds__(kT, 2) louver_probe_v5(const __grid_constant__
     }
     __syncthreads();
     // the exact kernel may start its own setup now (programmatic dependent launch)
+    if (vp.gmax && blockIdx.x == 0 && tid < G) {
+        const int ninf = __float_as_int(-INFINITY) ^ 0x7fffffff;  // order-preserving int of -inf
+        vp.gmax[(size_t)slot * G + tid] = ninf;
+    }
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     for (; tile < ntile; tile += stride) {
@@ -295,36 +300,52 @@ struct E5 {
 template <int DP, int G>
 __device__ void merge5(const float* src, int P, float* dst, float* out, float* part_out, int* counts,
                        float* shw) {
+    // shw: [P][G] weights, then M[G], L[G]; all partial headers are loaded in
+    // parallel and the o loads are batched, so a merge costs ~2 L2 round trips.
     const int tid = threadIdx.x;
     constexpr int W = G * (DP + 2);
+    float* shm = shw;              // [P][G] m, then weights
+    float* shl = shw + P * G;      // [P][G] l
+    float* ML = shl + P * G;       // M[G], L[G]
+    for (int i = tid; i < P * G; i += kT) {
+        const int s = i / G, g = i % G;
+        shm[i] = __ldcg(src + (size_t)s * W + g * (DP + 2));
+        shl[i] = __ldcg(src + (size_t)s * W + g * (DP + 2) + 1);
+    }
+    __syncthreads();
     if (tid < G) {
         float m = -INFINITY;
-        for (int s = 0; s < P; ++s) m = fmaxf(m, __ldcg(src + (size_t)s * W + tid * (DP + 2)));
+        for (int s = 0; s < P; ++s) m = fmaxf(m, shm[s * G + tid]);
         float l = 0.0f;
         for (int s = 0; s < P; ++s) {
-            const float ms = __ldcg(src + (size_t)s * W + tid * (DP + 2));
+            const float ms = shm[s * G + tid];
             const float w = ms == -INFINITY ? 0.0f : expf(ms - m);
-            shw[s * G + tid] = w;
-            l += w * __ldcg(src + (size_t)s * W + tid * (DP + 2) + 1);
+            shm[s * G + tid] = w;
+            l += w * shl[s * G + tid];
         }
-        shw[P * G + tid] = m;
-        shw[P * G + G + tid] = l;
+        ML[tid] = m;
+        ML[G + tid] = l;
     }
     __syncthreads();
     for (int i = tid; i < G * DP; i += kT) {
         const int g = i / DP, c = i % DP;
         float acc = 0.0f;
-        for (int s = 0; s < P; ++s) {
-            const float w = shw[s * G + g];
-            if (w != 0.0f) acc = fmaf(w, __ldcg(src + (size_t)s * W + g * (DP + 2) + 2 + c), acc);
+        for (int s0 = 0; s0 < P; s0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                v[j] = s0 + j < P ? __ldcg(src + (size_t)(s0 + j) * W + g * (DP + 2) + 2 + c) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j < P) acc = fmaf(shm[(s0 + j) * G + g], v[j], acc);
         }
-        const float l = shw[P * G + G + g];
+        const float l = ML[G + g];
         if (dst) dst[g * (DP + 2) + 2 + c] = acc;
         if (out) out[g * DP + c] = l > 0.0f ? acc / l : 0.0f;
         if (part_out) part_out[g * (DP + 2) + 2 + c] = acc;
     }
     if (tid < G) {
-        const float m = shw[P * G + tid], l = shw[P * G + G + tid];
+        const float m = ML[tid], l = ML[G + tid];
         if (dst) {
             dst[tid * (DP + 2)] = m;
             dst[tid * (DP + 2) + 1] = l;
@@ -337,356 +358,5 @@ __device__ void merge5(const float* src, int P, float* dst, float* out, float* p
     }
 }
 
-template <int DP, int G>
-__global__ void __launch_bounds__(kT, 2) louver_exact_v5(const __grid_constant__ V5Params vp) {
-    using Ge = E5<DP, G>;
-    const QueryParams& p = vp.p;
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint2* fr = reinterpret_cast<uint2*>(smem + Ge::OFF_FR);
-    float* qf = reinterpret_cast<float*>(smem + Ge::OFF_Q);
-    float* misc = reinterpret_cast<float*>(smem + Ge::OFF_M);
-    float* tau_s = misc;         // [G]
-    float* marg = misc + G;      // [G]
-    float* S = misc + 2 * G;     // [G]
-    float* red = misc + 4 * G;   // [kW*G]
-    int* iscr = reinterpret_cast<int*>(misc + 4 * G + kW * G);  // [8]
-    unsigned* klist = reinterpret_cast<unsigned*>(smem + Ge::OFF_KL);
-    unsigned* ucm = reinterpret_cast<unsigned*>(smem + Ge::FIXED);  // [tiles] masks
-    unsigned* upre = ucm + vp.tiles;                                // [tiles] exclusive row prefix
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int slot = blockIdx.y, blk = blockIdx.x;
-    unsigned char* ws = smem + Ge::OFF_WS + warp * Ge::WSZ;
-    float* ct = reinterpret_cast<float*>(ws);
-    float* wsc = ct + Ge::WCT;
-    const int q = lane & 3;
-    const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
-    const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
-
-    // ---- setup independent of the probe (overlaps it under programmatic launch)
-    setup_q<DP, G>(p.q + (size_t)slot * G * DP, p.colmax + (size_t)slot * DP, qf, red, S);
-    if (tid < G) {
-        tau_s[tid] = p.tau[(size_t)slot * G + tid];
-        marg[tid] = __fmul_ru(S[tid], 1.220703125e-4f);  // 2^-13 S
-    }
-    for (int i = tid; i < Ge::KS * Ge::NT * 32; i += kT) {
-        const int l = i & 31, nt = (i >> 5) % Ge::NT, t = (i >> 5) / Ge::NT;
-        fr[i] = b_frag<G, 3>(t, nt, l, [&](int k, int g) { return qf[g * (DP + 4) + k]; });
-    }
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // probe results visible from here
-
-    const long long n = p.ctr->n;
-    const long long indexed = p.ctr->indexed;
-    const int rl = p.r_log2, r = 1 << rl;
-    const long long ncells = (n + r - 1) >> rl;
-    const int ntile = (int)((ncells + 15) >> 4);
-    for (int u = tid; u < ntile; u += kT) ucm[u] = vp.cmask[(size_t)slot * vp.tiles + u];
-    __syncthreads();
-    {
-        const int per = (ntile + kT - 1) / kT;
-        const int u0 = tid * per;
-        int s = 0;
-        for (int u = u0; u < u0 + per && u < ntile; ++u) s += __popc(ucm[u]) << rl;
-        int incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) iscr[warp] = incl;
-        __syncthreads();
-        int basep = 0, total = 0;
-        for (int w = 0; w < kW; ++w) {
-            basep += w < warp ? iscr[w] : 0;
-            total += iscr[w];
-        }
-        int run = basep + incl - s;
-        for (int u = u0; u < u0 + per && u < ntile; ++u) {
-            upre[u] = (unsigned)run;
-            run += __popc(ucm[u]) << rl;
-        }
-        __syncthreads();
-        if (tid == 0) iscr[0] = total;
-        __syncthreads();
-    }
-    const long long total = iscr[0];
-    const long long lo = total * blk / vp.nb, hi = total * (blk + 1) / vp.nb;
-
-    // ---- per-warp online softmax state
-    constexpr int VPL = DP / 32;  // V dims per lane
-    float o[G][VPL], lsum[G], mrun[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        lsum[g] = 0.0f;
-        mrun[g] = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < VPL; ++e) o[g][e] = 0.0f;
-    }
-    int st_sel[G], st_att[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) st_sel[g] = st_att[g] = 0;
-    unsigned long long t_keys = 0, t_vals = 0;
-
-    for (long long seg = lo; seg < hi; seg += Ge::KL) {
-        const int nrow = (int)(hi - seg < Ge::KL ? hi - seg : Ge::KL);
-        // row -> key for the whole segment, all threads (unit by binary search, cell by bit select)
-        for (int i = tid; i < nrow; i += kT) {
-            const long long row = seg + i;
-            int a = 0, b = ntile - 1;
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if ((long long)upre[mid] <= row) a = mid; else b = mid - 1;
-            }
-            const int off = (int)(row - upre[a]);
-            unsigned m = ucm[a];
-            for (int j = 0; j < (off >> rl); ++j) m &= m - 1;
-            unsigned key = 0xffffffffu;
-            if (m != 0u) {
-                const long long kk = ((long long)a * 16 + (__ffs(m) - 1)) * r + (off & (r - 1));
-                if (kk >= 0 && kk < n) key = (unsigned)kk;
-            }
-            klist[i] = key;
-        }
-        if (tid == 0) iscr[1] = 0;
-        __syncthreads();
-        const int ntask = (nrow + 15) >> 4;
-        while (true) {
-            int task = 0;
-            if (lane == 0) task = atomicAdd(iscr + 1, 1);
-            task = __shfl_sync(0xffffffffu, task, 0);
-            if (task >= ntask) break;
-            const int r0i = task * 16;
-            const unsigned key = lane < 16 && r0i + lane < nrow ? klist[r0i + lane] : 0xffffffffu;
-            const unsigned k0 = __shfl_sync(0xffffffffu, key, lane >> 2);
-            const unsigned k1 = __shfl_sync(0xffffffffu, key, (lane >> 2) + 8);
-            const unsigned char* row0 =
-                reinterpret_cast<const unsigned char*>(Ks + (size_t)(k0 == 0xffffffffu ? 0 : k0) * DP);
-            const unsigned char* row1 =
-                reinterpret_cast<const unsigned char*>(Ks + (size_t)(k1 == 0xffffffffu ? 0 : k1) * DP);
-            constexpr int NP = DP / 32;
-            uint4 u0[NP], u1[NP];
-#pragma unroll
-            for (int pp = 0; pp < NP; ++pp) {
-                u0[pp] = ldg16(row0 + (32 * pp + 8 * q) * 2);
-                u1[pp] = ldg16(row1 + (32 * pp + 8 * q) * 2);
-            }
-            float acc[Ge::NT][4];
-#pragma unroll
-            for (int t = 0; t < Ge::NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
-#pragma unroll
-            for (int pp = 0; pp < NP; ++pp) {
-                const unsigned a0[4] = {u0[pp].x, u1[pp].x, u0[pp].y, u1[pp].y};
-                const unsigned a1[4] = {u0[pp].z, u1[pp].z, u0[pp].w, u1[pp].w};
-#pragma unroll
-                for (int t = 0; t < Ge::NT; ++t) {
-                    const uint2 b0 = fr[((2 * pp) * Ge::NT + t) * 32 + lane];
-                    const uint2 b1 = fr[((2 * pp + 1) * Ge::NT + t) * 32 + lane];
-                    mma16816(acc[t], a0, b0.x, b0.y);
-                    mma16816(acc[t], a1, b1.x, b1.y);
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < Ge::NT; ++t) {
-                const int rw = lane >> 2, col = t * 8 + 2 * q;
-                ct[rw * 8 * Ge::NT + col] = acc[t][0];
-                ct[rw * 8 * Ge::NT + col + 1] = acc[t][1];
-                ct[(rw + 8) * 8 * Ge::NT + col] = acc[t][2];
-                ct[(rw + 8) * 8 * Ge::NT + col + 1] = acc[t][3];
-            }
-            __syncwarp();
-            // classify (row, g): fast decides outside tau +- margin, else the normative dot
-            for (int pi = lane; pi < 16 * G; pi += 32) {
-                const int rw = pi / G, g = pi % G;
-                const unsigned kk = r0i + rw < nrow ? klist[r0i + rw] : 0xffffffffu;
-                float s = -INFINITY;
-                if (kk != 0xffffffffu) {
-                    const float* c = ct + rw * 8 * Ge::NT;
-                    float sc = (c[g] + c[G + g]) + c[2 * G + g];
-                    bool sel = sc >= tau_s[g] + marg[g];
-                    if (!sel && sc >= tau_s[g] - marg[g]) {  // undecided: normative dot (core.hpp:17-21)
-                        const unsigned char* kr = reinterpret_cast<const unsigned char*>(Ks + (size_t)kk * DP);
-                        const float* qg = qf + g * (DP + 4);
-                        float acc2 = 0.0f;
-                        for (int cc = 0; cc < DP / 8; ++cc) {
-                            const uint4 kv = ldg16(kr + cc * 16);
-                            float kf[8];
-                            lvk::unpack16<__nv_bfloat16>(kv, kf);
-#pragma unroll
-                            for (int e2 = 0; e2 < 8; ++e2) acc2 = __fadd_rn(acc2, __fmul_rn(qg[cc * 8 + e2], kf[e2]));
-                        }
-                        sc = acc2;
-                        sel = acc2 >= tau_s[g];
-                    }
-                    const bool in_buf = (long long)kk >= indexed;
-                    if (sel) {
-                        ++st_sel[g];
-                        if (p.bits) atomicOr(p.bits + ((size_t)slot * G + g) * p.bits_words + (kk >> 5), 1u << (kk & 31));
-                    }
-                    if (sel || (in_buf && !p.strict)) {
-                        s = sc;
-                        ++st_att[g];
-                    }
-                }
-                wsc[pi] = s;
-            }
-            __syncwarp();
-            // task max per q head (lane < 16 owns row lane), ILP over g
-            float sv[G], mx[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                sv[g] = lane < 16 ? wsc[lane * G + g] : -INFINITY;
-                mx[g] = sv[g] == -INFINITY ? -INFINITY : p.scale * sv[g];
-            }
-            bool att = false;
-#pragma unroll
-            for (int g = 0; g < G; ++g) att |= sv[g] != -INFINITY;
-            const unsigned amask = __ballot_sync(0xffffffffu, att) & 0xffffu;
-            const unsigned vkeys = __ballot_sync(0xffffffffu, key != 0xffffffffu);
-            if (lane == 0) t_keys += __popc(vkeys);
-            __syncwarp();
-            if (amask == 0) continue;
-            if (lane == 0) t_vals += __popc(amask);
-#pragma unroll
-            for (int of = 16; of > 0; of >>= 1)
-#pragma unroll
-                for (int g = 0; g < G; ++g) mx[g] = fmaxf(mx[g], __shfl_xor_sync(0xffffffffu, mx[g], of));
-            float pl[G], ls[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float mnew = fmaxf(mrun[g], mx[g]);
-                const float alpha = mrun[g] == -INFINITY ? 0.0f : __expf(mrun[g] - mnew);
-                mrun[g] = mnew;
-                lsum[g] *= alpha;
-#pragma unroll
-                for (int e = 0; e < VPL; ++e) o[g][e] *= alpha;
-                pl[g] = sv[g] == -INFINITY ? 0.0f : __expf(p.scale * sv[g] - mnew);
-                ls[g] = pl[g];
-            }
-#pragma unroll
-            for (int of = 16; of > 0; of >>= 1)
-#pragma unroll
-                for (int g = 0; g < G; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], of);
-#pragma unroll
-            for (int g = 0; g < G; ++g) lsum[g] += ls[g];
-            // V rows of attended keys, 8 per batch (8 bytes per lane at DP=128)
-            unsigned m = amask;
-            while (m) {
-                uint4 vv[8];
-                int rws[8];
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    rws[i] = -1;
-                    if (m) {
-                        const int rw = __ffs(m) - 1;
-                        m &= m - 1;
-                        rws[i] = rw;
-                        const unsigned kv = __shfl_sync(0xffffffffu, key, rw);
-                        vv[i] = ldg_v<VPL>(reinterpret_cast<const unsigned char*>(Vs + (size_t)kv * DP) + lane * VPL * 2);
-                        ++cnt;
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (i < cnt) {
-                        float vf[8];
-                        const unsigned vw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
-#pragma unroll
-                        for (int e = 0; e < VPL; ++e) vf[e] = (e & 1) ? lvk::bf_hi(vw[e >> 1]) : lvk::bf_lo(vw[e >> 1]);
-#pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            const float pw = __shfl_sync(0xffffffffu, pl[g], rws[i]);
-#pragma unroll
-                            for (int e = 0; e < VPL; ++e) o[g][e] = fmaf(pw, vf[e], o[g][e]);
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();  // klist is rewritten by the next segment
-    }
-
-    // ---- statistics
-    if (p.counts) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int s0 = lvk::warp_sum_int(st_sel[g]);
-            const int s1 = lvk::warp_sum_int(st_att[g]);
-            if (lane == 0) {
-                int* c = p.counts + ((size_t)slot * G + g) * 4;
-                if (s0) atomicAdd(c + 0, s0);
-                if (s1) atomicAdd(c + 1, s1);
-            }
-        }
-    }
-    if (p.totals && lane == 0) {
-        if (t_keys) atomicAdd(p.totals + 2, t_keys);
-        if (t_vals) atomicAdd(p.totals + 3, t_vals);
-    }
-
-    // ---- warp partials -> CTA partial
-    __syncthreads();
-    float* wred = reinterpret_cast<float*>(smem + Ge::OFF_WS);  // [kW][G][DP+2]
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        float* w = wred + (warp * G + g) * (DP + 2);
-        if (lane == 0) {
-            w[0] = mrun[g];
-            w[1] = lsum[g];
-        }
-#pragma unroll
-        for (int e = 0; e < VPL; ++e) w[2 + lane * VPL + e] = o[g][e];
-    }
-    __syncthreads();
-    constexpr int Wd = G * (DP + 2);
-    float* part = p.partial_ws + ((size_t)slot * vp.nb + blk) * Wd;
-    float* shw = reinterpret_cast<float*>(smem + Ge::OFF_KL);  // the key list is no longer needed
-    if (tid < G) {
-        float mm = -INFINITY;
-        for (int w = 0; w < kW; ++w) mm = fmaxf(mm, wred[(w * G + tid) * (DP + 2)]);
-        float l = 0.0f;
-        for (int w = 0; w < kW; ++w) {
-            const float mw = wred[(w * G + tid) * (DP + 2)];
-            const float a = mw == -INFINITY ? 0.0f : expf(mw - mm);
-            shw[w * G + tid] = a;
-            l += a * wred[(w * G + tid) * (DP + 2) + 1];
-        }
-        part[tid * (DP + 2)] = l > 0.0f ? mm : -INFINITY;
-        part[tid * (DP + 2) + 1] = l;
-    }
-    __syncthreads();
-    for (int i = tid; i < G * DP; i += kT) {
-        const int g = i / DP, c = i % DP;
-        float s = 0.0f;
-        for (int w = 0; w < kW; ++w) s = fmaf(shw[w * G + g], wred[(w * G + g) * (DP + 2) + 2 + c], s);
-        part[g * (DP + 2) + 2 + c] = s;
-    }
-
-    // ---- two-level merge
-    __threadfence();
-    __syncthreads();
-    int* flag = iscr + 4;
-    const int grp = blk / kMG;
-    const int members = vp.nb - grp * kMG < kMG ? vp.nb - grp * kMG : kMG;
-    if (tid == 0) *flag = atomicAdd(vp.gtickets + slot * vp.ngroups + grp, 1) == members - 1;
-    __syncthreads();
-    if (!*flag) return;
-    __threadfence();
-    merge5<DP, G>(p.partial_ws + ((size_t)slot * vp.nb + grp * kMG) * Wd, members,
-                  vp.gpart + ((size_t)slot * vp.ngroups + grp) * Wd, nullptr, nullptr, nullptr, shw);
-    if (tid == 0) vp.gtickets[slot * vp.ngroups + grp] = 0;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) *flag = atomicAdd(vp.stickets + slot, 1) == vp.ngroups - 1;
-    __syncthreads();
-    if (!*flag) return;
-    __threadfence();
-    merge5<DP, G>(vp.gpart + (size_t)slot * vp.ngroups * Wd, vp.ngroups, nullptr,
-                  p.out ? p.out + (size_t)slot * G * DP : nullptr,
-                  p.partial_out ? p.partial_out + (size_t)slot * Wd : nullptr,
-                  p.counts ? p.counts + (size_t)slot * G * 4 : nullptr, shw);
-    if (tid == 0) vp.stickets[slot] = 0;
-}
-
-cudaError_t launch_query_v5(int DP, int G, const V5Params& vp, int slots, cudaStream_t st);
 
 }  // namespace lvk5

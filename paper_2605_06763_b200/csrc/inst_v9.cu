@@ -1,0 +1,64 @@
+// bf16 query path, fused persistent layer kernel: DP in {64,128,256} x G in {1,2,4,8}.
+#include "louver_v9.cuh"
+
+namespace lvk9 {
+
+template <int DP, int G>
+static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st) {
+    using Ge = C9<DP, G>;
+    static int smem_set = 0;
+    static int occ = 0;
+    const int ngrp = (vp.tiles + 31) / 32;
+    const int smem = Ge::smem(ngrp);
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(louver_layer_v9<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, louver_layer_v9<DP, G>, Ge::NTHR, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+        smem_set = smem;
+    }
+    // every CTA of a slot's team must be resident (per-slot barrier): size the
+    // grid to one wave and let it loop over slots if there are more
+    const int cap = occ * sms;
+    int nb = cap / slots;
+    if (nb > vp.nb) nb = vp.nb;  // workspace holds vp.nb partials per slot
+    if (nb < 1) nb = 1;
+    int gy = cap / nb;
+    if (gy > slots) gy = slots;
+    vp.nb = nb;
+    vp.slots = slots;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)nb, (unsigned)gy);
+    cfg.blockDim = dim3(Ge::NTHR);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G>, vp);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st) {
+#define LV9_G(D)                                              \
+    switch (G) {                                              \
+        case 1: return launch_t<D, 1>(vp, slots, sms, st);    \
+        case 2: return launch_t<D, 2>(vp, slots, sms, st);    \
+        case 4: return launch_t<D, 4>(vp, slots, sms, st);    \
+        case 8: return launch_t<D, 8>(vp, slots, sms, st);    \
+    }                                                         \
+    break;
+    switch (DP) {
+        case 64: LV9_G(64)
+        case 128: LV9_G(128)
+        case 256: LV9_G(256)
+    }
+#undef LV9_G
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace lvk9

@@ -16,6 +16,8 @@
 #include "louver_dispatch.h"
 #include "louver_v2.cuh"
 #include "louver_v7.cuh"
+#include "louver_v8.cuh"
+#include "louver_v9.cuh"
 
 using lvk::Counters;
 
@@ -66,6 +68,7 @@ struct lv_ctx {
     int DP = 0, G = 1, r = 1, r_log2 = 0, slots = 0, rows = 0;
     long long cap = 0, cap_cells = 0, bits_words = 0;
     int splits = 1, chunks_per_split = 1, ngroups = 1;
+    int sms = 148;
     int nb = 1, nb_groups = 1, units = 1;  // bf16: score/attend CTAs per slot, merge groups, 512-key units
     int nbp = 1;                           // bf16: probe CTAs per slot
     void* K = nullptr;
@@ -156,6 +159,7 @@ void choose_splits(lv_ctx* c) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        c->sms = sms;
         long long nb = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
         c->nb = (int)std::min<long long>(nb, 4096);
@@ -303,7 +307,10 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         v5.ngroups = c->nb_groups;
         v5.gmax = nullptr;
         v5.p.tot_trace = c->trace;
-        e = lvk7::launch_query_v7(c->DP, c->G, v5, c->slots, st);
+        static const int k2 = [] { const char* e = getenv("LV_K2"); return e ? atoi(e) : 9; }();
+        if (k2 == 7) e = lvk7::launch_query_v7(c->DP, c->G, v5, c->slots, st);
+        else if (k2 == 8) e = lvk8::launch_query_v8(c->DP, c->G, v5, c->slots, st);
+        else e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st);
     } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
         lvk2::V2Params vp{};
         vp.p = p;

@@ -51,6 +51,7 @@ struct V5Params {
     int* stickets;             // [slots]
     int ngroups;
     int* gmax;                 // optional [slot][G]: reset to the encoding of -inf by K1
+    int slots;                 // v9: slots of the layer (the grid may loop over them)
 };
 
 // physical element of logical (k-step t, fragment element e in 0..3) for lane q:

@@ -1,0 +1,794 @@
+// Louver bf16 query path as ONE persistent kernel per layer (sm_100a).
+//
+// Per slot (batch x kv head) a fixed team of CTAs, all co-resident (cooperative
+// launch), runs three phases:
+//
+//   A  probe      cell summaries [hi | lo] (16 cells = one block) are scored
+//                 against [q+ | q-] on the tensor cores; a cell survives for head g
+//                 iff its box bound reaches tau_g - 2^-12 S_g (sound: bf16 split
+//                 error << the margin). Survivor bits go to a per-slot mask.
+//                 (reference: Louver.probe, louver.cpp / core.hpp gate bounds)
+//   --  per-slot barrier (counter in L2; every CTA of the slot is resident)
+//   B  exact      the slot's surviving cells are split evenly over the team; each
+//      + attend   16-key task is scored on the tensor cores (q in three bf16
+//                 parts), pairs within 2^-13 S_g of tau settled with the
+//                 normative sequential fp32 dot (core.hpp:17-21); the V rows of
+//                 the attended keys (selected ∪ buffer unless strict,
+//                 cache.cpp:48-68) are folded in with P.V on the tensor cores
+//                 (P split in two bf16 parts, V bf16 exact).
+//   C  merge      (m, l, o) partials of the team, combined by the last CTA.
+//
+// Every block of keys, summaries or values moves global -> shared with cp.async
+// into a per-warp 3-stage ring, 128-byte XOR swizzle (chunk ^ row&7), read with
+// ldmatrix, so no register holds an in-flight block and the fragments need no
+// register shuffling. Per warp the exact phase is a software pipeline:
+// K(t+1) in flight | K(t) scored | V(t-1) in flight, folded after K(t) is scored.
+#pragma once
+
+#include "louver_v5.cuh"
+
+namespace lvk9 {
+
+using lvk::QueryParams;
+using lvk5::V5Params;
+using lvk2::mma16816;
+
+__device__ __forceinline__ void cpa16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa16z(unsigned dst, const void* src, bool valid) {  // zero-fill if !valid
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void ldsm4(unsigned (&r)[4], unsigned a) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ void ldsm4t(unsigned (&r)[4], unsigned a) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds16(unsigned a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(a)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned bf2(float lo, float hi) {
+    return (unsigned)lvk2::bf_bits(lo) | ((unsigned)lvk2::bf_bits(hi) << 16);
+}
+
+// B fragment (k = 16 ks + 2q + (e&1) + 8(e>>1), n = nt*8 + lane/4) of a k-way
+// bf16 split: column n is part n / G of head g = n % G.
+template <int G, int PARTS, typename Val>
+__device__ __forceinline__ uint2 b_nat(int ks, int nt, int lane, Val val) {
+    const int col = nt * 8 + lane / 4, q = lane & 3;
+    unsigned short v[4] = {0, 0, 0, 0};
+    if (col < PARTS * G) {
+        const int part = col / G, g = col % G;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float x = val(16 * ks + 2 * q + (e & 1) + 8 * (e >> 1), g);
+            unsigned short b = lvk2::bf_bits(x);
+            for (int k = 0; k < part; ++k) {
+                x = x - lvk2::bf_val(b);
+                b = lvk2::bf_bits(x);
+            }
+            v[e] = b;
+        }
+    }
+    return make_uint2((unsigned)v[0] | ((unsigned)v[1] << 16), (unsigned)v[2] | ((unsigned)v[3] << 16));
+}
+
+template <int DP, int G>
+struct C9 {
+    static constexpr int NT = (3 * G + 7) / 8;   // exact: n-tiles of [q0|q1|q2]
+    static constexpr int NTP = (2 * G + 7) / 8;  // probe: n-tiles of [p0|p1]
+    static constexpr int KS = DP / 16;
+    static constexpr int CPR = DP / 8;           // 16-byte chunks per row
+    static constexpr int RB = DP * 2;            // bytes per bf16 row
+    static constexpr int STAGE = 16 * RB;
+    static constexpr int PPL = G >= 2 ? G / 2 : 1;
+    static constexpr int MT = DP / 16;           // P.V m-tiles (16 dims each)
+    static constexpr int CT = 8 * (NT > NTP ? NT : NTP);  // C tile row pitch (floats)
+    static constexpr int CL = 1024;              // surviving cells per list segment
+    static constexpr int MINB = DP <= 128 ? 2 : 1;
+    static constexpr int SZ_FRE = KS * NT * 32 * 8;
+    static constexpr int SZ_FRP = 2 * KS * NTP * 32 * 8;
+    static constexpr int OFF_FRE = 0;
+    static constexpr int OFF_FRP = OFF_FRE + SZ_FRE;
+    static constexpr int OFF_Q = OFF_FRP + SZ_FRP;                    // [G][DP+4] f32
+    static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
+    static constexpr int MISC = 5 * G + 8 * G + 32;
+    static constexpr int OFF_CL = (OFF_M + MISC * 4 + 15) / 16 * 16;  // [CL] cell ids
+    static constexpr int FIX = (OFF_CL + CL * 4 + 127) / 128 * 128;
+    static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
+    static constexpr int BUDGET = MINB == 2 ? 112 * 1024 : 224 * 1024;
+    static constexpr int NW0 = (BUDGET - FIX) / PERW;
+    static constexpr int NW = NW0 > 8 ? 8 : NW0;
+    static constexpr int NTHR = NW * 32;
+    static constexpr int OFF_W = FIX;                                 // per-warp areas
+    static constexpr int DYN = OFF_W + NW * PERW;                     // then [ngrp] gsum, [ngrp] gpre
+    static int smem(int ngrp) { return DYN + ngrp * 8; }
+    static_assert(NW >= 2, "Louver v9: shared memory budget too small");
+};
+
+template <int DP, int G>
+__global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ V5Params vp) {
+    using Ge = C9<DP, G>;
+    constexpr int NW = Ge::NW, NTHR = Ge::NTHR, NT = Ge::NT, NTP = Ge::NTP, KS = Ge::KS, CPR = Ge::CPR,
+                  RB = Ge::RB, PPL = Ge::PPL, MT = Ge::MT, CT = Ge::CT;
+    const QueryParams& p = vp.p;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint2* fre = reinterpret_cast<uint2*>(smem + Ge::OFF_FRE);
+    uint2* frp = reinterpret_cast<uint2*>(smem + Ge::OFF_FRP);
+    float* qf = reinterpret_cast<float*>(smem + Ge::OFF_Q);
+    float* misc = reinterpret_cast<float*>(smem + Ge::OFF_M);
+    float* tau_s = misc;               // [G]
+    float* taup_s = misc + G;          // [G] probe threshold tau - 2^-12 S
+    float* marg_s = misc + 2 * G;      // [G] 2^-13 S
+    float* S_s = misc + 3 * G;         // [G]
+    float* red = misc + 5 * G;         // [8 G]
+    int* iscr = reinterpret_cast<int*>(misc + 13 * G);  // [32]
+    unsigned* clist = reinterpret_cast<unsigned*>(smem + Ge::OFF_CL);
+    int* gsum = reinterpret_cast<int*>(smem + Ge::DYN);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int blk = blockIdx.x, nb = vp.nb;
+    unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
+    const unsigned ring = lvk2::smem_u32(wbase);
+    float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
+    float* pbuf = ct + 16 * CT;
+    const int q4 = lane & 3;
+    // per-lane ldmatrix offsets: A (rows = keys / cells) and V^T (trans)
+    const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
+    const unsigned a_off = a_row * RB;
+    const int v_row = (lane & 7) + 8 * (lane >> 4), v_hi = (lane >> 3) & 1;
+    const unsigned v_off = v_row * RB;
+
+    long long* trace = nullptr;
+#define LV9_TRACE(i) \
+    if (trace && tid == 0) trace[i] = lvk2::gtimer();
+
+    // zero the ring once: rows of a V stage that are not loaded meet P = 0
+    for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
+        *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+
+    for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
+        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 16 : nullptr;
+        LV9_TRACE(0)
+        const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
+        const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
+        const unsigned char* sumb =
+            reinterpret_cast<const unsigned char*>(vp.sum + (size_t)slot * p.cap_cells * (2 * DP));
+        unsigned short* cmask = vp.cmask + (size_t)slot * vp.tiles;
+
+        // ---- phase A prologue: the first summary blocks depend on nothing
+        const int wg = blk * NW + warp, pstride = nb * NW;
+        auto p_issue = [&](int u, int bound) {  // sub-task u: tile wg + (u>>1) pstride, half u&1 ([hi] or [lo])
+            const int tile = wg + (u >> 1) * pstride;
+            if (tile < bound) {
+                const unsigned char* src = sumb + ((size_t)tile * 16 * (2 * DP) + (u & 1) * DP) * 2;
+                const unsigned dst = ring + (u % 3) * Ge::STAGE;
+#pragma unroll
+                for (int k = 0; k < CPR / 2; ++k) {
+                    const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
+                    cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), src + row * (2 * RB) + c * 16);
+                }
+            }
+            cpa_commit();
+        };
+        p_issue(0, vp.tiles);
+        p_issue(1, vp.tiles);
+
+        // ---- setup: q, S_g, thresholds, B fragments
+        {
+            const float* qsrc = p.q + (size_t)slot * G * DP;
+            const float* colmax = p.colmax + (size_t)slot * DP;
+            float s[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) s[g] = 0.0f;
+            for (int i = tid; i < G * DP; i += NTHR) {
+                const int g = i / DP, c = i % DP;
+                const float x = qsrc[i];
+                qf[g * (DP + 4) + c] = x;
+                const float t = __fmul_ru(fabsf(x), colmax[c]);
+#pragma unroll
+                for (int h = 0; h < G; ++h)
+                    if (h == g) s[h] = __fadd_ru(s[h], t);
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float v = s[g];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v = __fadd_ru(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == 0) red[warp * G + g] = v;
+            }
+            __syncthreads();
+            if (tid < G) {
+                float v = 0.0f;
+                for (int w = 0; w < NW; ++w) v = __fadd_ru(v, red[w * G + tid]);
+                const float tau = p.tau[(size_t)slot * G + tid];
+                S_s[tid] = v;
+                tau_s[tid] = tau;
+                taup_s[tid] = __fsub_rd(tau, __fmul_ru(v, 2.44140625e-4f));  // 2^-12 S
+                marg_s[tid] = __fmul_ru(v, 1.220703125e-4f);                 // 2^-13 S
+            }
+            for (int i = tid; i < KS * NT * 32; i += NTHR) {
+                const int l = i & 31, nt = (i >> 5) % NT, ks = (i >> 5) / NT;
+                fre[i] = b_nat<G, 3>(ks, nt, l, [&](int k, int g) { return qf[g * (DP + 4) + k]; });
+            }
+            for (int i = tid; i < 2 * KS * NTP * 32; i += NTHR) {
+                const int l = i & 31, nt = (i >> 5) % NTP, ks = ((i >> 5) / NTP) % KS, h = (i >> 5) / (NTP * KS);
+                frp[i] = b_nat<G, 2>(ks, nt, l, [&](int k, int g) {
+                    const float x = qf[g * (DP + 4) + k];
+                    return h == 0 ? fmaxf(x, 0.0f) : fminf(x, 0.0f);  // [hi | lo] . [q+ | q-]
+                });
+            }
+            __syncthreads();
+        }
+        LV9_TRACE(1)
+        const long long n = p.ctr->n;
+        const long long indexed = p.ctr->indexed;
+        const int rl = p.r_log2, r = 1 << rl;
+        const long long ncells = (n + r - 1) >> rl;
+        const int ntile = (int)((ncells + 15) >> 4);
+
+        // ---- phase A: probe
+        {
+            float taup[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) taup[g] = taup_s[g];
+            float acc[NTP][4];
+            for (int u = 0;; ++u) {
+                const int tile = wg + (u >> 1) * pstride;
+                if (tile >= ntile) break;
+                p_issue(u + 2, ntile);
+                cpa_wait<2>();
+                __syncwarp();
+                const int half = u & 1;
+                if (half == 0) {
+#pragma unroll
+                    for (int nt = 0; nt < NTP; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
+                }
+                const unsigned sb = ring + (u % 3) * Ge::STAGE + a_off;
+                const uint2* fh = frp + half * KS * NTP * 32;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    unsigned a[4];
+                    ldsm4(a, sb + (((2 * ks + a_hi) ^ (a_row & 7)) << 4));
+#pragma unroll
+                    for (int nt = 0; nt < NTP; ++nt) {
+                        const uint2 b = fh[(ks * NTP + nt) * 32 + lane];
+                        mma16816(acc[nt], a, b.x, b.y);
+                    }
+                }
+                if (half == 1) {
+#pragma unroll
+                    for (int nt = 0; nt < NTP; ++nt) {
+                        const int rw = lane >> 2, col = nt * 8 + 2 * q4;
+                        *reinterpret_cast<float2*>(ct + rw * CT + col) = make_float2(acc[nt][0], acc[nt][1]);
+                        *reinterpret_cast<float2*>(ct + (rw + 8) * CT + col) = make_float2(acc[nt][2], acc[nt][3]);
+                    }
+                    __syncwarp();
+                    unsigned gm = 0;
+                    int scan = 0;
+                    const long long cell = ((long long)tile << 4) + lane;
+                    if (lane < 16 && cell < ncells) {
+                        const long long cs = cell << rl, ce = cs + r;
+                        if (ce > indexed) {
+                            gm = (1u << G) - 1u;  // holds buffer keys: scanned densely
+                        } else {
+#pragma unroll
+                            for (int g = 0; g < G; ++g)
+                                if (ct[lane * CT + g] + ct[lane * CT + G + g] >= taup[g]) gm |= 1u << g;
+                        }
+                        scan = (int)((ce < n ? ce : n) - cs);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, gm != 0) & 0xffffu;
+                    if (lane == 0) cmask[tile] = (unsigned short)m;
+                    if (p.totals) {
+                        const int tested = __popc(__ballot_sync(0xffffffffu, lane < 16 && cell < ncells));
+                        if (lane == 0) {
+                            atomicAdd(p.totals + 0, (unsigned long long)tested);
+                            atomicAdd(p.totals + 1, (unsigned long long)__popc(m));
+                        }
+                    }
+                    if (p.counts) {
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const int v = lvk::warp_sum_int((gm >> g) & 1 ? scan : 0);
+                            if (lane == 0 && v) atomicAdd(p.counts + ((size_t)slot * G + g) * 4 + 2, v);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            cpa_wait<0>();
+            __syncwarp();
+        }
+        LV9_TRACE(2)
+
+        // ---- per-slot barrier: every CTA of the team has published its masks
+        int* bar = vp.gtickets + (size_t)slot * vp.ngroups;
+        __threadfence();  // this thread's mask writes, before the team counter
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd(bar, 1);
+            while (ld_acquire(bar) < nb) __nanosleep(64);
+        }
+        __syncthreads();
+        LV9_TRACE(3)
+
+        // ---- surviving cells: per 32-tile group counts, exclusive prefix
+        const int ngrp = (ntile + 31) >> 5;
+        int* gpre = gsum + ngrp;
+        for (int gi = warp; gi < ngrp; gi += NW) {
+            const int tile = gi * 32 + lane;
+            const unsigned m = tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
+            const int s = __reduce_add_sync(0xffffffffu, (unsigned)__popc(m));
+            if (lane == 0) gsum[gi] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int carry = 0;
+            for (int g0 = 0; g0 < ngrp; g0 += 32) {
+                const int v = g0 + lane < ngrp ? gsum[g0 + lane] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (g0 + lane < ngrp) gpre[g0 + lane] = carry + incl - v;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) iscr[0] = carry;
+        }
+        __syncthreads();
+        const long long cs_total = iscr[0];
+        const long long c_lo = cs_total * blk / nb, c_hi = cs_total * (blk + 1) / nb;
+        LV9_TRACE(4)
+
+        // ---- phase B: exact + attend
+        const int g_me = lane % G;
+        const float tau_me = tau_s[g_me], marg_me = marg_s[g_me];
+        const float* q_me = qf + g_me * (DP + 4);
+        const float scale = p.scale;
+        const int tpc_l2 = rl - 4;  // log2(16-row tasks per cell)
+        float o[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.0f;
+        float mrun = -INFINITY, lpart = 0.0f;
+        int my_sel = 0, my_att = 0;
+        unsigned long long t_keys = 0, t_vals = 0;
+
+        for (long long seg = c_lo; seg < c_hi; seg += Ge::CL) {
+            const long long seg_end = c_hi - seg < Ge::CL ? c_hi : seg + Ge::CL;
+            const int ncell = (int)(seg_end - seg);
+            for (int gi = warp; gi < ngrp; gi += NW) {  // cell ids of surviving cells [seg, seg_end)
+                const long long g_lo = gpre[gi];
+                if (g_lo >= seg_end || g_lo + gsum[gi] <= seg) continue;
+                const int tile = gi * 32 + lane;
+                unsigned m = tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
+                const int cnt = __popc(m);
+                int incl = cnt;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o2);
+                    if (lane >= o2) incl += t;
+                }
+                long long ci = g_lo + incl - cnt;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (ci >= seg && ci < seg_end) clist[ci - seg] = (unsigned)(tile * 16 + b);
+                    ++ci;
+                }
+            }
+            __syncthreads();
+            const int ntask = ncell << tpc_l2;
+            auto key0 = [&](int t) -> long long {
+                return ((long long)clist[t >> tpc_l2] << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
+            };
+            auto k_issue = [&](int t, int stage) {  // rows past n land as zeros
+                if (t < ntask) {
+                    const long long kb = key0(t);
+                    const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks + (size_t)kb * DP);
+                    const unsigned dst = ring + stage * Ge::STAGE;
+#pragma unroll
+                    for (int k = 0; k < CPR / 2; ++k) {
+                        const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
+                        cpa16z(dst + row * RB + ((c ^ (row & 7)) << 4), src + row * RB + c * 16, kb + row < n);
+                    }
+                }
+                cpa_commit();
+            };
+            int t = warp, st = 0;
+            bool pend = false;
+            unsigned pb[4] = {0u, 0u, 0u, 0u};  // B fragments of the pending task's P (hi b0 b1, lo b0 b1)
+            k_issue(t, 0);
+            cpa_commit();  // stands for V(t-1)
+            for (; t < ntask; t += NW) {
+                const int s1 = st == 2 ? 0 : st + 1;
+                const int s2 = st == 0 ? 2 : st - 1;  // stage of V(t-1)
+                const long long k0 = key0(t);
+                k_issue(t + NW, s1);
+                cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
+                __syncwarp();
+                // -- scores: 16 keys x [q0|q1|q2] per head
+                const unsigned sb = ring + st * Ge::STAGE;
+                {
+                    float acc[NT][4];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        unsigned a[4];
+                        ldsm4(a, sb + a_off + (((2 * ks + a_hi) ^ (a_row & 7)) << 4));
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            const uint2 b = fre[(ks * NT + nt) * 32 + lane];
+                            mma16816(acc[nt], a, b.x, b.y);
+                        }
+                    }
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const int rw = lane >> 2, col = nt * 8 + 2 * q4;
+                        *reinterpret_cast<float2*>(ct + rw * CT + col) = make_float2(acc[nt][0], acc[nt][1]);
+                        *reinterpret_cast<float2*>(ct + (rw + 8) * CT + col) = make_float2(acc[nt][2], acc[nt][3]);
+                    }
+                }
+                __syncwarp();
+                // -- classify this lane's pairs (row pi / G, head g_me)
+                float s[PPL];
+                unsigned und = 0, selb = 0;
+#pragma unroll
+                for (int j = 0; j < PPL; ++j) {
+                    const int pi = lane + 32 * j, rw = pi / G;
+                    const float* c = ct + (rw < 16 ? rw : 15) * CT;
+                    const float sc = (c[g_me] + c[G + g_me]) + c[2 * G + g_me];
+                    const bool valid = (G > 1 || lane < 16) && k0 + rw < n;
+                    const bool sel = valid && sc >= tau_me + marg_me;
+                    const bool u = valid && !sel && sc >= tau_me - marg_me;
+                    s[j] = sc;
+                    und |= (unsigned)u << j;
+                    selb |= (unsigned)sel << j;
+                }
+                if (__any_sync(0xffffffffu, und != 0)) {  // rare: the normative sequential dot
+#pragma unroll
+                    for (int j = 0; j < PPL; ++j) {
+                        if ((und >> j) & 1) {
+                            const int rw = (lane + 32 * j) / G;
+                            const unsigned rb = sb + rw * RB;
+                            float a2 = 0.0f;
+#pragma unroll 1
+                            for (int cc = 0; cc < CPR; ++cc) {
+                                const uint4 kv = lds16(rb + ((cc ^ (rw & 7)) << 4));
+                                float kf[8];
+                                lvk::unpack16<__nv_bfloat16>(kv, kf);
+#pragma unroll
+                                for (int e2 = 0; e2 < 8; ++e2) a2 = __fadd_rn(a2, __fmul_rn(q_me[cc * 8 + e2], kf[e2]));
+                            }
+                            s[j] = a2;
+                            if (a2 >= tau_me) selb |= 1u << j;
+                        }
+                    }
+                }
+                unsigned amask = 0;  // rows with any attended head
+                float mloc = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < PPL; ++j) {
+                    const int pi = lane + 32 * j, rw = pi / G;
+                    const long long kk = k0 + rw;
+                    const bool valid = (G > 1 || lane < 16) && kk < n;
+                    const bool sel = (selb >> j) & 1;
+                    if (sel) {
+                        ++my_sel;
+                        if (p.bits)
+                            atomicOr(p.bits + ((size_t)slot * G + g_me) * p.bits_words + (kk >> 5), 1u << (kk & 31));
+                    }
+                    const bool att = sel || (valid && !p.strict && kk >= indexed);
+                    my_att += att;
+                    s[j] = att ? scale * s[j] : -INFINITY;
+                    mloc = fmaxf(mloc, s[j]);
+                    // row any-head flag: OR over the G lanes of the row, then one lane per row
+                    unsigned any = att;
+#pragma unroll
+                    for (int of = 1; of < G; of <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, of);
+                    const unsigned b = __ballot_sync(0xffffffffu, any && g_me == 0);
+                    // bits at lanes k*G -> rows j*(32/G) + k
+#pragma unroll
+                    for (int k = 0; k < 32 / G && k < 16; ++k) amask |= ((b >> (k * G)) & 1u) << (j * (32 / G) + k);
+                }
+                if (lane == 0) t_keys += (k0 + 16 <= n) ? 16 : (n > k0 ? n - k0 : 0);
+                float alpha = 1.0f;
+                unsigned nbf[4] = {0u, 0u, 0u, 0u};
+                if (amask) {
+                    if (lane == 0) t_vals += __popc(amask);
+#pragma unroll
+                    for (int of = 16; of >= G; of >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, of));
+                    const float mnew = fmaxf(mrun, mloc);
+                    alpha = mrun == -INFINITY ? 0.0f : __expf(mrun - mnew);
+                    mrun = mnew;
+                    float lp = lpart * alpha;
+#pragma unroll
+                    for (int j = 0; j < PPL; ++j) {
+                        const float pv = s[j] == -INFINITY ? 0.0f : __expf(s[j] - mnew);
+                        lp += pv;
+                        if (G > 1 || lane < 16) pbuf[lane + 32 * j] = pv;
+                    }
+                    lpart = lp;
+                    __syncwarp();
+                    // B fragment of P: k = rows (2q, 2q+1 | 2q+8, 2q+9), n = head lane/4
+                    const int hn = lane >> 2;
+                    float pv4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                    if (hn < G) {
+                        pv4[0] = pbuf[(2 * q4) * G + hn];
+                        pv4[1] = pbuf[(2 * q4 + 1) * G + hn];
+                        pv4[2] = pbuf[(2 * q4 + 8) * G + hn];
+                        pv4[3] = pbuf[(2 * q4 + 9) * G + hn];
+                    }
+                    float lo4[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) lo4[e] = pv4[e] - lvk2::bf_val(lvk2::bf_bits(pv4[e]));
+                    nbf[0] = bf2(pv4[0], pv4[1]);
+                    nbf[1] = bf2(pv4[2], pv4[3]);
+                    nbf[2] = bf2(lo4[0], lo4[1]);
+                    nbf[3] = bf2(lo4[2], lo4[3]);
+                }
+                __syncwarp();  // K(t) and pbuf reads done
+                // -- V(t): attended rows into K(t)'s stage (same row positions)
+                if (amask) {
+                    constexpr int RPI = 32 / CPR;  // rows per warp instruction
+                    unsigned mm = amask;
+                    const unsigned dst = ring + st * Ge::STAGE;
+                    const int sub = lane / CPR, c = lane % CPR;
+                    while (mm) {
+                        int rsel = -1;
+#pragma unroll
+                        for (int k = 0; k < RPI; ++k) {
+                            const int rr = mm ? __ffs(mm) - 1 : -1;
+                            mm &= mm - 1;
+                            if (k == sub) rsel = rr;
+                        }
+                        if (rsel >= 0)
+                            cpa16(dst + rsel * RB + ((c ^ (rsel & 7)) << 4),
+                                  reinterpret_cast<const unsigned char*>(Vs + (size_t)(k0 + rsel) * DP) + c * 16);
+                    }
+                }
+                cpa_commit();
+                // -- fold V(t-1) (frame m_{t-1}), then move o to frame m_t
+                cpa_wait<2>();  // V(t-1) landed (K(t+1), V(t) may pend)
+                __syncwarp();
+                if (pend) {
+                    const unsigned vb = ring + s2 * Ge::STAGE + v_off;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        unsigned a[4];
+                        ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
+                        mma16816(o[mt], a, pb[0], pb[1]);
+                        mma16816(o[mt], a, pb[2], pb[3]);
+                    }
+                }
+                if (amask) {
+                    const float a0 = __shfl_sync(0xffffffffu, alpha, (2 * q4) % G);
+                    const float a1 = __shfl_sync(0xffffffffu, alpha, (2 * q4 + 1) % G);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        o[mt][0] *= a0;
+                        o[mt][1] *= a1;
+                        o[mt][2] *= a0;
+                        o[mt][3] *= a1;
+                    }
+                }
+                pend = amask != 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) pb[e] = nbf[e];
+                st = s1;
+            }
+            cpa_wait<0>();
+            __syncwarp();
+            if (pend) {  // the last task's V
+                const int s2 = st == 0 ? 2 : st - 1;
+                const unsigned vb = ring + s2 * Ge::STAGE + v_off;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    unsigned a[4];
+                    ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
+                    mma16816(o[mt], a, pb[0], pb[1]);
+                    mma16816(o[mt], a, pb[2], pb[3]);
+                }
+            }
+            __syncwarp();
+            __syncthreads();  // clist is rewritten by the next segment
+        }
+        LV9_TRACE(5)
+
+        // ---- statistics: lanes with the same g = lane % G hold that head's counts
+        if (p.counts) {
+            int s0 = my_sel, s1 = my_att;
+#pragma unroll
+            for (int of = 16; of >= G; of >>= 1) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, of);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, of);
+            }
+            if (lane < G) {
+                int* c = p.counts + ((size_t)slot * G + lane) * 4;
+                if (s0) atomicAdd(c + 0, s0);
+                if (s1) atomicAdd(c + 1, s1);
+            }
+        }
+        if (p.totals && lane == 0) {
+            if (t_keys) atomicAdd(p.totals + 2, t_keys);
+            if (t_vals) atomicAdd(p.totals + 3, t_vals);
+        }
+#pragma unroll
+        for (int of = 16; of >= G; of >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, of);
+
+        // ---- warp partials -> CTA partial [G][DP+2] (m, l, o)
+        constexpr int Wd = G * (DP + 2);
+        float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Wd] over the rings
+        float* shw = red;                                           // [NW][G] weights
+        __syncthreads();
+        {
+            float* w = wred + warp * Wd;
+            if (lane < G) {
+                w[lane * (DP + 2)] = mrun;
+                w[lane * (DP + 2) + 1] = lpart;
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int h = 2 * q4 + (e & 1), c = 16 * mt + (lane >> 2) + 8 * (e >> 1);
+                    if (h < G) w[h * (DP + 2) + 2 + c] = o[mt][e];
+                }
+            }
+        }
+        __syncthreads();
+        float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wd;
+        if (tid < G) {
+            float mm = -INFINITY;
+            for (int w = 0; w < NW; ++w) mm = fmaxf(mm, wred[w * Wd + tid * (DP + 2)]);
+            float l = 0.0f;
+            for (int w = 0; w < NW; ++w) {
+                const float mw = wred[w * Wd + tid * (DP + 2)];
+                const float a = mw == -INFINITY ? 0.0f : __expf(mw - mm);
+                shw[w * G + tid] = a;
+                l += a * wred[w * Wd + tid * (DP + 2) + 1];
+            }
+            part[tid * (DP + 2)] = l > 0.0f ? mm : -INFINITY;
+            part[tid * (DP + 2) + 1] = l;
+        }
+        __syncthreads();
+        for (int i = tid; i < G * DP; i += NTHR) {
+            const int g = i / DP, c = i % DP;
+            float s = 0.0f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * Wd + g * (DP + 2) + 2 + c], s);
+            part[g * (DP + 2) + 2 + c] = s;
+        }
+        LV9_TRACE(6)
+
+        // ---- phase C: the last CTA of the team merges the nb partials
+        int* ticket = vp.stickets + slot;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            iscr[1] = atomicAdd(ticket, 1) == nb - 1;
+        }
+        __syncthreads();
+        if (iscr[1]) {
+            __threadfence();
+            LV9_TRACE(8)
+            const float* src = p.partial_ws + (size_t)slot * nb * Wd;
+            // scratch over the rings: M[G], L[G], m/weights [nb][G], l [nb][G], then the o chunks
+            float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);
+            float* L = M + G;
+            float* wgt = M + 2 * G;
+            float* lsv = wgt + nb * G;
+            const int hdr = (2 * G + 2 * nb * G + 3) / 4 * 4;
+            constexpr int EPT = (G * DP + NTHR - 1) / NTHR;
+            float accr[EPT];
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) accr[k] = 0.0f;
+            // headers: one round trip
+            for (int i = tid; i < nb * G; i += NTHR) {
+                const float* h = src + (size_t)(i / G) * Wd + (i % G) * (DP + 2);
+                wgt[i] = __ldcg(h);
+                lsv[i] = __ldcg(h + 1);
+            }
+            __syncthreads();
+            if (tid < G) {
+                float mm = -INFINITY;
+                for (int s2 = 0; s2 < nb; ++s2) mm = fmaxf(mm, wgt[s2 * G + tid]);
+                M[tid] = mm;
+            }
+            __syncthreads();
+            for (int i = tid; i < nb * G; i += NTHR) {
+                const float ms = wgt[i];
+                wgt[i] = ms == -INFINITY ? 0.0f : __expf(ms - M[i % G]);
+            }
+            __syncthreads();
+            if (tid < G) {
+                float l = 0.0f;
+                for (int s2 = 0; s2 < nb; ++s2) l += wgt[s2 * G + tid] * lsv[s2 * G + tid];
+                L[tid] = l;
+            }
+            // o rows through the rings, a chunk of partials per round trip
+            const int per_chunk = (NW * Ge::PERW - hdr * 4) / (Wd * 4);
+            float* stage = M + hdr;
+            const unsigned stage_u = lvk2::smem_u32(stage);
+            for (int s0 = 0; s0 < nb; s0 += per_chunk) {
+                const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
+                const float* cs = src + (size_t)s0 * Wd;
+                for (int i = tid; i < cnt * Wd / 2; i += NTHR) {
+                    const unsigned d = stage_u + i * 8;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(cs + 2 * i) : "memory");
+                }
+                cpa_commit();
+                cpa_wait<0>();
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    const int i = tid + k * NTHR;
+                    if (i < G * DP) {
+                        const int g = i / DP, c = i % DP;
+                        float a = accr[k];
+                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stage[s2 * Wd + g * (DP + 2) + 2 + c], a);
+                        accr[k] = a;
+                    }
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                const int i = tid + k * NTHR;
+                if (i < G * DP) {
+                    const int g = i / DP, c = i % DP;
+                    const float l = L[g];
+                    if (p.out) p.out[((size_t)slot * G + g) * DP + c] = l > 0.0f ? accr[k] / l : 0.0f;
+                    if (p.partial_out) p.partial_out[(size_t)slot * Wd + g * (DP + 2) + 2 + c] = accr[k];
+                }
+            }
+            if (tid < G) {
+                if (p.partial_out) {
+                    p.partial_out[(size_t)slot * Wd + tid * (DP + 2)] = L[tid] > 0.0f ? M[tid] : -INFINITY;
+                    p.partial_out[(size_t)slot * Wd + tid * (DP + 2) + 1] = L[tid];
+                }
+                if (p.counts) p.counts[((size_t)slot * G + tid) * 4 + 3] = L[tid] > 0.0f ? 1 : 0;
+            }
+            if (tid == 0) {
+                *ticket = 0;
+                *bar = 0;
+            }
+            LV9_TRACE(7)
+        }
+        __syncthreads();
+        // the ring was used as merge scratch: restore zeros for the next slot
+        for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
+            *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+    }
+#undef LV9_TRACE
+}
+
+cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st);
+
+}  // namespace lvk9

@@ -45,12 +45,12 @@ def main():
     layer._ctx.lib.lv_debug_trace(layer._ctx.h, None)
     print(f"event time of traced query: {st.elapsed_time(en) * 1e3:.1f} us")
     tr = buf.cpu().numpy().astype(np.float64)
-    cnt = tr[:, 8:14].sum(0)
-    print(f"cycles (sum over warps): mma+wait {cnt[0]:.3e} classify {cnt[1]:.3e} attend {cnt[2]:.3e}; "
-          f"undecided pairs {cnt[3]:.0f}, tasks {cnt[4]:.0f}, V rows {cnt[5]:.0f}")
-    print(f"per task cycles: mma {cnt[0]/cnt[4]:.0f} cls {cnt[1]/cnt[4]:.0f} att {cnt[2]/cnt[4]:.0f}")
-    tr = tr[:, :8]
     t0 = tr[:, 0].min()
+    fin = tr[tr[:, 7] > 0]
+    for row in fin:
+        r = (row - t0) / 1e3
+        print(f"  final CTA: partial {r[6]:.2f} ticket1 {r[8]:.2f} merge1 {r[9]:.2f} ticket2 {r[10]:.2f} end {r[7]:.2f}")
+    tr = tr[:, :8]
     rel = (tr - t0) / 1e3
     names = ["setup", "wait", "prefix", "cells", "tasks", "partial", "merge"]
     print(f"CTAs {len(tr)}; start spread {rel[:, 0].max():.2f} us; last end {rel[:, 7].max():.2f} us")

@@ -69,30 +69,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_release(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned bf2(float lo, float hi) {
     return (unsigned)lvk2::bf_bits(lo) | ((unsigned)lvk2::bf_bits(hi) << 16);
-}
-
-// B fragment (k = 16 ks + 2q + (e&1) + 8(e>>1), n = nt*8 + lane/4) of a k-way
-// bf16 split: column n is part n / G of head g = n % G.
-template <int G, int PARTS, typename Val>
-__device__ __forceinline__ uint2 b_nat(int ks, int nt, int lane, Val val) {
-    const int col = nt * 8 + lane / 4, q = lane & 3;
-    unsigned short v[4] = {0, 0, 0, 0};
-    if (col < PARTS * G) {
-        const int part = col / G, g = col % G;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            float x = val(16 * ks + 2 * q + (e & 1) + 8 * (e >> 1), g);
-            unsigned short b = lvk2::bf_bits(x);
-            for (int k = 0; k < part; ++k) {
-                x = x - lvk2::bf_val(b);
-                b = lvk2::bf_bits(x);
-            }
-            v[e] = b;
-        }
-    }
-    return make_uint2((unsigned)v[0] | ((unsigned)v[1] << 16), (unsigned)v[2] | ((unsigned)v[3] << 16));
 }
 
 template <int DP, int G>
@@ -124,7 +110,8 @@ struct C9 {
     static constexpr int NTHR = NW * 32;
     static constexpr int OFF_W = FIX;                                 // per-warp areas
     static constexpr int DYN = OFF_W + NW * PERW;                     // then [ngrp] gsum, [ngrp] gpre
-    static int smem(int ngrp) { return DYN + ngrp * 8; }
+    static constexpr int MCG = 64;                                    // cache masks in smem up to 64 groups
+    static int smem(int ngrp) { return DYN + ngrp * 8 + (ngrp <= MCG ? ngrp * 64 : 0); }
     static_assert(NW >= 2, "Louver v9: shared memory budget too small");
 };
 
@@ -196,21 +183,39 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         p_issue(0, vp.tiles);
         p_issue(1, vp.tiles);
 
-        // ---- setup: q, S_g, thresholds, B fragments
+        // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip)
+        const long long n = __ldcg(&p.ctr->n);
+        const long long indexed = __ldcg(&p.ctr->indexed);
         {
             const float* qsrc = p.q + (size_t)slot * G * DP;
             const float* colmax = p.colmax + (size_t)slot * DP;
+            constexpr int QPT = (G * DP + NTHR - 1) / NTHR;
+            float xq[QPT], xc[QPT];
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) {
+                const int i = tid + k * NTHR;
+                xq[k] = i < G * DP ? __ldg(qsrc + i) : 0.0f;
+                xc[k] = i < G * DP ? __ldg(colmax + i % DP) : 0.0f;
+            }
+            const float tau_r = tid < G ? __ldg(p.tau + (size_t)slot * G + tid) : 0.0f;
+            // zero the fragment arrays (columns past PARTS * G stay zero)
+            for (int i = tid; i < (Ge::SZ_FRE + Ge::SZ_FRP) / 16; i += NTHR)
+                reinterpret_cast<uint4*>(smem + Ge::OFF_FRE)[i] = make_uint4(0u, 0u, 0u, 0u);
             float s[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) s[g] = 0.0f;
-            for (int i = tid; i < G * DP; i += NTHR) {
-                const int g = i / DP, c = i % DP;
-                const float x = qsrc[i];
-                qf[g * (DP + 4) + c] = x;
-                const float t = __fmul_ru(fabsf(x), colmax[c]);
+            if (trace && tid == 0) trace[9] = lvk2::gtimer() + (long long)(xq[0] * 0.0f);
 #pragma unroll
-                for (int h = 0; h < G; ++h)
-                    if (h == g) s[h] = __fadd_ru(s[h], t);
+            for (int k = 0; k < QPT; ++k) {
+                const int i = tid + k * NTHR;
+                if (i < G * DP) {
+                    const int g = i / DP, c = i % DP;
+                    qf[g * (DP + 4) + c] = xq[k];
+                    const float t = __fmul_ru(fabsf(xq[k]), xc[k]);
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+                        if (h == g) s[h] = __fadd_ru(s[h], t);
+                }
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -223,28 +228,48 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             if (tid < G) {
                 float v = 0.0f;
                 for (int w = 0; w < NW; ++w) v = __fadd_ru(v, red[w * G + tid]);
-                const float tau = p.tau[(size_t)slot * G + tid];
+                const float tau = tau_r;
                 S_s[tid] = v;
                 tau_s[tid] = tau;
                 taup_s[tid] = __fsub_rd(tau, __fmul_ru(v, 2.44140625e-4f));  // 2^-12 S
                 marg_s[tid] = __fmul_ru(v, 1.220703125e-4f);                 // 2^-13 S
             }
-            for (int i = tid; i < KS * NT * 32; i += NTHR) {
-                const int l = i & 31, nt = (i >> 5) % NT, ks = (i >> 5) / NT;
-                fre[i] = b_nat<G, 3>(ks, nt, l, [&](int k, int g) { return qf[g * (DP + 4) + k]; });
-            }
-            for (int i = tid; i < 2 * KS * NTP * 32; i += NTHR) {
-                const int l = i & 31, nt = (i >> 5) % NTP, ks = ((i >> 5) / NTP) % KS, h = (i >> 5) / (NTP * KS);
-                frp[i] = b_nat<G, 2>(ks, nt, l, [&](int k, int g) {
-                    const float x = qf[g * (DP + 4) + k];
-                    return h == 0 ? fmaxf(x, 0.0f) : fminf(x, 0.0f);  // [hi | lo] . [q+ | q-]
-                });
+            LV9_TRACE(10)
+            // each q element scatters its bf16 split parts straight into the B fragments:
+            // element k of head g, part P sits in column P G + g; within a k-step of 16,
+            // r = k % 16 -> lane quad (r & 7) / 2, half e = (r & 1) | (r >> 3) << 1
+            unsigned short* fe = reinterpret_cast<unsigned short*>(fre);
+            unsigned short* fp = reinterpret_cast<unsigned short*>(frp);
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) {
+                const int i = tid + k * NTHR;
+                if (i < G * DP) {
+                    const int g = i / DP, c = i % DP;
+                    const int ks = c >> 4, rr = c & 15, e = (rr & 1) | ((rr >> 3) << 1), qq = (rr & 7) >> 1;
+                    float y = xq[k];
+#pragma unroll
+                    for (int P = 0; P < 3; ++P) {
+                        const unsigned short b = lvk2::bf_bits(y);
+                        y -= lvk2::bf_val(b);
+                        const int col = P * G + g;
+                        fe[((ks * NT + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float z = h == 0 ? fmaxf(xq[k], 0.0f) : fminf(xq[k], 0.0f);  // [hi | lo] . [q+ | q-]
+#pragma unroll
+                        for (int P = 0; P < 2; ++P) {
+                            const unsigned short b = lvk2::bf_bits(z);
+                            z -= lvk2::bf_val(b);
+                            const int col = P * G + g;
+                            fp[(((h * KS + ks) * NTP + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
+                        }
+                    }
+                }
             }
             __syncthreads();
         }
         LV9_TRACE(1)
-        const long long n = p.ctr->n;
-        const long long indexed = p.ctr->indexed;
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
         const int ntile = (int)((ncells + 15) >> 4);
@@ -326,21 +351,23 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         // ---- per-slot barrier: every CTA of the team has published its masks
         int* bar = vp.gtickets + (size_t)slot * vp.ngroups;
-        __threadfence();  // this thread's mask writes, before the team counter
-        __syncthreads();
+        __syncthreads();  // the team's mask writes are ordered before the release below
         if (tid == 0) {
-            atomicAdd(bar, 1);
-            while (ld_acquire(bar) < nb) __nanosleep(64);
+            red_release(bar, 1);
+            while (ld_acquire(bar) < nb) __nanosleep(32);
         }
         __syncthreads();
         LV9_TRACE(3)
 
         // ---- surviving cells: per 32-tile group counts, exclusive prefix
         const int ngrp = (ntile + 31) >> 5;
-        int* gpre = gsum + ngrp;
+        const int ngrp_cap = (vp.tiles + 31) >> 5;  // the dynamic smem layout
+        int* gpre = gsum + ngrp_cap;
+        unsigned short* mcache = ngrp_cap <= Ge::MCG ? reinterpret_cast<unsigned short*>(gpre + ngrp_cap) : nullptr;
         for (int gi = warp; gi < ngrp; gi += NW) {
             const int tile = gi * 32 + lane;
             const unsigned m = tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
+            if (mcache) mcache[tile] = (unsigned short)m;
             const int s = __reduce_add_sync(0xffffffffu, (unsigned)__popc(m));
             if (lane == 0) gsum[gi] = s;
         }
@@ -385,7 +412,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 const long long g_lo = gpre[gi];
                 if (g_lo >= seg_end || g_lo + gsum[gi] <= seg) continue;
                 const int tile = gi * 32 + lane;
-                unsigned m = tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
+                unsigned m = mcache ? (unsigned)mcache[tile] : tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
                 const int cnt = __popc(m);
                 int incl = cnt;
 #pragma unroll
@@ -523,13 +550,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     if (lane == 0) t_vals += __popc(amask);
 #pragma unroll
                     for (int of = 16; of >= G; of >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, of));
-                    const float mnew = fmaxf(mrun, mloc);
-                    alpha = mrun == -INFINITY ? 0.0f : __expf(mrun - mnew);
-                    mrun = mnew;
+                    // lazy rescale: the reference max moves only when a score exceeds it by
+                    // more than 8 (weights stay <= e^8); o and l are rescaled only then
+                    if (mloc > mrun + 8.0f) {
+                        alpha = mrun == -INFINITY ? 0.0f : __expf(mrun - mloc);
+                        mrun = mloc;
+                    }
                     float lp = lpart * alpha;
 #pragma unroll
                     for (int j = 0; j < PPL; ++j) {
-                        const float pv = s[j] == -INFINITY ? 0.0f : __expf(s[j] - mnew);
+                        const float pv = s[j] == -INFINITY ? 0.0f : __expf(s[j] - mrun);
                         lp += pv;
                         if (G > 1 || lane < 16) pbuf[lane + 32 * j] = pv;
                     }
@@ -586,7 +616,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         mma16816(o[mt], a, pb[2], pb[3]);
                     }
                 }
-                if (amask) {
+                if (__any_sync(0xffffffffu, alpha != 1.0f)) {
                     const float a0 = __shfl_sync(0xffffffffu, alpha, (2 * q4) % G);
                     const float a1 = __shfl_sync(0xffffffffu, alpha, (2 * q4 + 1) % G);
 #pragma unroll
@@ -688,14 +718,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         // ---- phase C: the last CTA of the team merges the nb partials
         int* ticket = vp.stickets + slot;
-        __threadfence();
         __syncthreads();
-        if (tid == 0) {
-            iscr[1] = atomicAdd(ticket, 1) == nb - 1;
-        }
+        if (tid == 0) iscr[1] = atom_add_acq_rel(ticket, 1) == nb - 1;
         __syncthreads();
         if (iscr[1]) {
-            __threadfence();
             LV9_TRACE(8)
             const float* src = p.partial_ws + (size_t)slot * nb * Wd;
             // scratch over the rings: M[G], L[G], m/weights [nb][G], l [nb][G], then the o chunks
@@ -708,34 +734,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             float accr[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) accr[k] = 0.0f;
-            // headers: one round trip
-            for (int i = tid; i < nb * G; i += NTHR) {
-                const float* h = src + (size_t)(i / G) * Wd + (i % G) * (DP + 2);
-                wgt[i] = __ldcg(h);
-                lsv[i] = __ldcg(h + 1);
-            }
-            __syncthreads();
-            if (tid < G) {
-                float mm = -INFINITY;
-                for (int s2 = 0; s2 < nb; ++s2) mm = fmaxf(mm, wgt[s2 * G + tid]);
-                M[tid] = mm;
-            }
-            __syncthreads();
-            for (int i = tid; i < nb * G; i += NTHR) {
-                const float ms = wgt[i];
-                wgt[i] = ms == -INFINITY ? 0.0f : __expf(ms - M[i % G]);
-            }
-            __syncthreads();
-            if (tid < G) {
-                float l = 0.0f;
-                for (int s2 = 0; s2 < nb; ++s2) l += wgt[s2 * G + tid] * lsv[s2 * G + tid];
-                L[tid] = l;
-            }
-            // o rows through the rings, a chunk of partials per round trip
             const int per_chunk = (NW * Ge::PERW - hdr * 4) / (Wd * 4);
             float* stage = M + hdr;
             const unsigned stage_u = lvk2::smem_u32(stage);
-            for (int s0 = 0; s0 < nb; s0 += per_chunk) {
+            auto chunk_issue = [&](int s0) {
                 const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
                 const float* cs = src + (size_t)s0 * Wd;
                 for (int i = tid; i < cnt * Wd / 2; i += NTHR) {
@@ -743,20 +745,57 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(cs + 2 * i) : "memory");
                 }
                 cpa_commit();
+            };
+            chunk_issue(0);  // the first chunk of o rows travels with the headers
+            // headers: one round trip
+            for (int i = tid; i < nb * G; i += NTHR) {
+                const float* h = src + (size_t)(i / G) * Wd + (i % G) * (DP + 2);
+                wgt[i] = __ldcg(h);
+                lsv[i] = __ldcg(h + 1);
+            }
+            __syncthreads();
+            LV9_TRACE(11)
+            for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
+                float mm = -INFINITY;
+                for (int s2 = lane; s2 < nb; s2 += 32) mm = fmaxf(mm, wgt[s2 * G + g]);
+#pragma unroll
+                for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
+                float l = 0.0f;
+                for (int s2 = lane; s2 < nb; s2 += 32) {
+                    const float ms = wgt[s2 * G + g];
+                    const float w = ms == -INFINITY ? 0.0f : __expf(ms - mm);
+                    wgt[s2 * G + g] = w;
+                    l += w * lsv[s2 * G + g];
+                }
+#pragma unroll
+                for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+                if (lane == 0) {
+                    M[g] = mm;
+                    L[g] = l;
+                }
+            }
+            __syncthreads();
+            // o rows through the rings, a chunk of partials per round trip
+            for (int s0 = 0; s0 < nb; s0 += per_chunk) {
+                const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
+                if (s0 > 0) chunk_issue(s0);
                 cpa_wait<0>();
                 __syncthreads();
+                LV9_TRACE(13)
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int i = tid + k * NTHR;
                     if (i < G * DP) {
                         const int g = i / DP, c = i % DP;
                         float a = accr[k];
+#pragma unroll 8
                         for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stage[s2 * Wd + g * (DP + 2) + 2 + c], a);
                         accr[k] = a;
                     }
                 }
                 __syncthreads();
             }
+            LV9_TRACE(14)
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 const int i = tid + k * NTHR;

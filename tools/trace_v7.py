@@ -49,7 +49,11 @@ def main():
     fin = tr[tr[:, 7] > 0]
     for row in fin:
         r = (row - t0) / 1e3
-        print(f"  final CTA: partial {r[6]:.2f} ticket1 {r[8]:.2f} merge1 {r[9]:.2f} ticket2 {r[10]:.2f} end {r[7]:.2f}")
+        print(f"  final CTA: partial {r[6]:.2f} won {r[8]:.2f} headers {r[11]:.2f} weights {r[12]:.2f} "
+              f"chunk {r[13]:.2f} acc {r[14]:.2f} end {r[7]:.2f}")
+    for i, nm in ((9, "q loaded"), (10, "S ready"), (1, "frags done")):
+        v = (tr[:, i] - t0) / 1e3
+        print(f"  setup {nm:10s} quantiles " + " ".join(f"{x:6.2f}" for x in np.percentile(v, [0, 50, 100])))
     tr = tr[:, :8]
     rel = (tr - t0) / 1e3
     names = ["setup", "wait", "prefix", "cells", "tasks", "partial", "merge"]

@@ -142,11 +142,17 @@ int lv_query(lv_ctx* ctx, const lv_query_args* args);
 size_t lv_query_workspace_bytes(const lv_ctx* ctx);
 
 /* Device geometry: out[8] = {padded d, cell keys r, arena rows, cells per slot,
- * query splits per slot, chunks per split, keys per chunk, query smem bytes}. */
+ * query splits per slot, chunks per split, keys per chunk, query smem bytes}
+ * (the split geometry of the fp32 / dense / brute-force kernels). */
 int lv_geometry(const lv_ctx* ctx, int64_t* out);
 
-/* Debug: while dev_buf != NULL, bf16 queries write 8 globaltimer stamps per
- * CTA (grid order [slot][split]) into dev_buf [slots*splits][8]. */
+/* bf16 query path (one fused persistent kernel per layer): out[4] = {CTAs per
+ * slot, resident CTAs per SM, threads per CTA, dynamic smem bytes} as chosen
+ * by the last query launch; zeros before the first bf16 query. */
+int lv_layer_geometry(const lv_ctx* ctx, int64_t* out);
+
+/* Debug: while dev_buf != NULL, bf16 queries write 16 globaltimer stamps per
+ * CTA (order [slot][team CTA]) into dev_buf [slots*team][16]. */
 int lv_debug_trace(lv_ctx* ctx, int64_t* dev_buf);
 int64_t lv_bitmap_words(const lv_ctx* ctx);
 

@@ -85,6 +85,7 @@ _SIGS = {
     "lv_query_workspace_bytes": (C.c_size_t, [_P]),
     "lv_geometry": (C.c_int, [_P, _P]),
     "lv_debug_trace": (C.c_int, [_P, _P]),
+    "lv_layer_geometry": (C.c_int, [_P, _P]),
     "lv_bitmap_words": (C.c_int64, [_P]),
     "lv_n": (C.c_int64, [_P]),
     "lv_indexed_count": (C.c_int64, [_P]),

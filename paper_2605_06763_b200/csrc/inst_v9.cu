@@ -4,7 +4,7 @@
 namespace lvk9 {
 
 template <int DP, int G>
-static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st) {
+static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, int* geo) {
     using Ge = C9<DP, G>;
     static int smem_set = 0;
     static int occ = 0;
@@ -28,6 +28,12 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st) {
     if (gy > slots) gy = slots;
     vp.nb = nb;
     vp.slots = slots;
+    if (geo) {  // team CTAs per slot, threads per CTA, dynamic smem, resident CTAs per SM
+        geo[0] = nb;
+        geo[1] = Ge::NTHR;
+        geo[2] = smem;
+        geo[3] = occ;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)nb, (unsigned)gy);
     cfg.blockDim = dim3(Ge::NTHR);
@@ -43,13 +49,13 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st) {
+cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st, int* geo) {
 #define LV9_G(D)                                              \
     switch (G) {                                              \
-        case 1: return launch_t<D, 1>(vp, slots, sms, st);    \
-        case 2: return launch_t<D, 2>(vp, slots, sms, st);    \
-        case 4: return launch_t<D, 4>(vp, slots, sms, st);    \
-        case 8: return launch_t<D, 8>(vp, slots, sms, st);    \
+        case 1: return launch_t<D, 1>(vp, slots, sms, st, geo);    \
+        case 2: return launch_t<D, 2>(vp, slots, sms, st, geo);    \
+        case 4: return launch_t<D, 4>(vp, slots, sms, st, geo);    \
+        case 8: return launch_t<D, 8>(vp, slots, sms, st, geo);    \
     }                                                         \
     break;
     switch (DP) {

@@ -69,6 +69,7 @@ struct lv_ctx {
     long long cap = 0, cap_cells = 0, bits_words = 0;
     int splits = 1, chunks_per_split = 1, ngroups = 1;
     int sms = 148;
+    int layer_geo[4] = {0, 0, 0, 0};  // fused bf16 layer kernel: team CTAs/slot, threads, smem, CTAs/SM
     int nb = 1, nb_groups = 1, units = 1;  // bf16: score/attend CTAs per slot, merge groups, 512-key units
     int nbp = 1;                           // bf16: probe CTAs per slot
     void* K = nullptr;
@@ -310,7 +311,7 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         static const int k2 = [] { const char* e = getenv("LV_K2"); return e ? atoi(e) : 9; }();
         if (k2 == 7) e = lvk7::launch_query_v7(c->DP, c->G, v5, c->slots, st);
         else if (k2 == 8) e = lvk8::launch_query_v8(c->DP, c->G, v5, c->slots, st);
-        else e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st);
+        else e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
     } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
         lvk2::V2Params vp{};
         vp.p = p;
@@ -482,6 +483,14 @@ int lv_geometry(const lv_ctx* c, int64_t* out) {
     out[6] = lvk::kChunk;
     out[7] = c->cfg.dtype == LV_BF16 ? lvk2::query_v2_smem(c->DP, c->G)
                                      : lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
+    return LV_OK;
+}
+int lv_layer_geometry(const lv_ctx* c, int64_t* out) {
+    if (!c || !out) return fail(LV_EINVAL, "lv_layer_geometry: null argument");
+    out[0] = c->layer_geo[0];  // CTAs per slot (team)
+    out[1] = c->layer_geo[3];  // resident CTAs per SM
+    out[2] = c->layer_geo[1];  // threads per CTA
+    out[3] = c->layer_geo[2];  // dynamic shared memory bytes
     return LV_OK;
 }
 int64_t lv_bitmap_words(const lv_ctx* c) { return c ? c->bits_words : 0; }

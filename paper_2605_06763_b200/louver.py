@@ -375,7 +375,13 @@ class LouverLayer:
         check(self._ctx.lib.lv_geometry(self._ctx.h, g.ctypes.data), "lv_geometry")
         keys = ("dp", "cell_keys", "arena_rows", "cells", "splits", "chunks_per_split", "chunk_keys",
                 "smem_bytes")
-        return {k: int(v) for k, v in zip(keys, g)}
+        out = {k: int(v) for k, v in zip(keys, g)}
+        if self.dtype == LV_BF16:  # the fused layer kernel's launch geometry (after a query)
+            lg = np.zeros((4,), np.int64)
+            check(self._ctx.lib.lv_layer_geometry(self._ctx.h, lg.ctypes.data), "lv_layer_geometry")
+            out.update(zip(("team_ctas_per_slot", "ctas_per_sm", "threads_per_cta", "layer_smem_bytes"),
+                           (int(v) for v in lg)))
+        return out
 
     def build(self, K, V, stream=None) -> None:
         """K, V: [batch][H_kv][n][d] fp32 or bf16 (numpy host or torch cuda)."""

@@ -1,0 +1,403 @@
+// louver_b200.hpp — C++20 host layer over the C ABI (louver_b200.h).
+//
+// Mirrors the reference library's public API (namespace `louver`, headers under
+// /root/reference/proj/include/louver/) so a C++ caller of the reference can
+// switch by changing the namespace and linking liblouver_b200.so:
+//
+//   louver::BuildConfig / validate         index.hpp:10-22          -> BuildConfig
+//   louver::KeyStore                       core.hpp:116-169         -> KeyStore (host rows, used to adopt)
+//   louver::QueryRequest / QueryStats      query.hpp:11-30          -> QueryRequest / QueryStats
+//   louver::AttentionResult                query.hpp:37-41          -> AttentionResult
+//   louver::FilterAlgo / CacheQueryResult  cache.hpp:7-16           -> FilterAlgo / CacheQueryResult
+//   louver::LouverCache                    cache.hpp:21-63          -> LouverCache (device-resident store + index)
+//   louver::brute_force_range              query.hpp:44-45          -> brute_force_range(const LouverCache&, ...)
+//   louver::sparse_attention               query.hpp:69-72          -> sparse_attention(const LouverCache&, ...)
+//
+// Differences a caller sees: the store lives in HBM inside the cache, so the
+// free functions take the cache instead of a `const KeyStore&`; `index()` is not
+// exposed (the device index is cell summaries, not the reference's groups).
+// Errors are the reference's: std::invalid_argument, std::out_of_range,
+// std::runtime_error; an empty attention set is std::nullopt and an empty flush
+// returns false.
+//
+// The multi-head decode layer (batch x H_kv slots, GQA, bf16 KV, device
+// pointers, one fused kernel per query) is `LouverLayer`; sharded partials are
+// combined with `lse_merge`.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "louver_b200.h"
+
+namespace louver_b200 {
+
+using KeyId = std::uint32_t;  // types.hpp:14
+using Scalar = float;
+using Vector = std::vector<Scalar>;
+using ConstVecRef = std::span<const Scalar>;
+
+namespace detail {
+inline int check(int rc, const char* what) {
+    if (rc >= 0) return rc;  // LV_OK or LV_EMPTY
+    std::string msg = std::string(what) + ": " + lv_last_error();
+    switch (rc) {
+        case LV_EINVAL: throw std::invalid_argument(msg);
+        case LV_ERANGE: throw std::out_of_range(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+// device scratch owned by one call
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+        if (bytes) cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
+    }
+    ~DevBuf() { if (p) cudaFree(p); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+struct CtxDeleter {
+    void operator()(lv_ctx* c) const { lv_destroy(c); }
+};
+}  // namespace detail
+
+// index.hpp:13-20
+enum class Grouping { Contiguous = 0, Interleaved = 1, Random = 2, PcaTree = 3 };
+enum class EnclosureKind { Ball = 0, Aabb = 1, SpanBall = 2 };
+
+// index.hpp:10-22. On the device keys are grouped into contiguous cells of r keys
+// (r rounded up to a power of two, <= 64) with AABB summaries; S, grouping and
+// enclosing are validated like the reference and change pruning, never results.
+struct BuildConfig {
+    std::size_t S = 4;
+    std::size_t r = 4;
+    Grouping grouping = Grouping::PcaTree;
+    EnclosureKind enclosing = EnclosureKind::Ball;
+    std::uint64_t rng_seed = 0;
+
+    void validate(int d) const {
+        if (S < 1) throw std::invalid_argument("BuildConfig: S >= 1 required");
+        if (r < 1) throw std::invalid_argument("BuildConfig: r >= 1 required");
+        if (S > static_cast<std::size_t>(d)) throw std::invalid_argument("BuildConfig: S <= d required");
+    }
+};
+
+// core.hpp:116-169: append-only host rows (keys and values), used to adopt a prefill.
+class KeyStore {
+  public:
+    explicit KeyStore(int dim) : dim_(dim) {
+        if (dim < 1) throw std::invalid_argument("KeyStore: dimension >= 1 required");
+    }
+    KeyStore(std::vector<Scalar> keys, std::vector<Scalar> values, int dim)
+        : dim_(dim), keys_(std::move(keys)), values_(std::move(values)) {
+        if (dim < 1) throw std::invalid_argument("KeyStore: dimension >= 1 required");
+        if (keys_.size() != values_.size() || keys_.size() % dim)
+            throw std::invalid_argument("KeyStore: keys/values shape mismatch");
+    }
+    KeyId append(ConstVecRef k, ConstVecRef v) {
+        if (k.size() != static_cast<size_t>(dim_) || v.size() != static_cast<size_t>(dim_))
+            throw std::invalid_argument("KeyStore::append: dimension mismatch");
+        keys_.insert(keys_.end(), k.begin(), k.end());
+        values_.insert(values_.end(), v.begin(), v.end());
+        return static_cast<KeyId>(n() - 1);
+    }
+    int dim() const { return dim_; }
+    std::size_t n() const { return keys_.size() / dim_; }
+    ConstVecRef key(KeyId j) const { return {keys_.data() + static_cast<size_t>(j) * dim_, static_cast<size_t>(dim_)}; }
+    ConstVecRef value(KeyId j) const { return {values_.data() + static_cast<size_t>(j) * dim_, static_cast<size_t>(dim_)}; }
+    const Scalar* key_data() const { return keys_.data(); }
+    const Scalar* value_data() const { return values_.data(); }
+
+  private:
+    int dim_;
+    std::vector<Scalar> keys_, values_;
+};
+
+// query.hpp:11-19
+struct QueryRequest {
+    Vector q;
+    Scalar tau = 0.0f;
+    std::optional<std::vector<Scalar>> tau_subspace;  // accepted; the device probe derives its own bounds
+    Scalar scale = 0.0f;                              // 0 means 1/sqrt(d)
+
+    Scalar effective_scale() const {
+        return scale != 0.0f ? scale : Scalar(1.0 / std::sqrt(double(q.size())));
+    }
+};
+
+// query.hpp:21-30 (device meaning: groups = cells of r keys)
+struct QueryStats {
+    std::int64_t groups_tested = 0;  // cells whose bound was evaluated
+    std::int64_t keys_scanned = 0;   // keys entering the exact check (surviving cells + buffer)
+    double f_scan = 0.0;             // keys_scanned / n
+    double gate_cost_equiv = 0.0;    // 2 * groups_tested / r (AABB: hi and lo rows)
+};
+
+// query.hpp:37-41
+struct AttentionResult {
+    std::vector<KeyId> selected_ids;
+    std::vector<Scalar> weights;  // aligned with selected_ids (filled by sparse_attention)
+    Vector output;
+};
+
+// cache.hpp:7-16
+enum class FilterAlgo { FullSubspace = LV_ALGO_FULL_SUBSPACE, Ta = LV_ALGO_TA };
+
+struct CacheQueryResult {
+    std::vector<KeyId> selected;   // all keys meeting the threshold, ascending
+    std::vector<KeyId> retrieved;  // selected ∪ buffer
+    QueryStats stats;
+    std::optional<AttentionResult> attention;
+};
+
+// cache.hpp:21-63: one head, fp32 KV in HBM, device index + update buffer of
+// capacity B (auto-flush at B). Single writer; const queries may run
+// concurrently (each call uses its own device workspace).
+class LouverCache {
+  public:
+    LouverCache(int dim, BuildConfig cfg, std::size_t buffer_capacity, std::size_t capacity = 1024)
+        : dim_(dim), cfg_(cfg), buffer_capacity_(buffer_capacity) {
+        cfg.validate(dim);
+        if (buffer_capacity < 1) throw std::invalid_argument("LouverCache: buffer capacity >= 1 required");
+        create(capacity < 16 ? 16 : capacity);
+    }
+
+    // Adopts an existing store; all of it is indexed immediately (cache.hpp:31-36).
+    LouverCache(const KeyStore& store, BuildConfig cfg, std::size_t buffer_capacity)
+        : dim_(store.dim()), cfg_(cfg), buffer_capacity_(buffer_capacity) {
+        if (buffer_capacity < 1) throw std::invalid_argument("LouverCache: buffer capacity >= 1 required");
+        cfg.validate(dim_);
+        create(store.n() * 2 < 1024 ? 1024 : store.n() * 2);
+        if (store.n())
+            detail::check(lv_build(ctx_.get(), store.key_data(), store.value_data(), (int64_t)store.n(), LV_F32,
+                                   LV_HOST, nullptr),
+                          "lv_build");
+    }
+
+    void push_key(ConstVecRef k, ConstVecRef v) {
+        if (k.size() != static_cast<size_t>(dim_) || v.size() != static_cast<size_t>(dim_))
+            throw std::invalid_argument("KeyStore::append: dimension mismatch");
+        if (n() >= capacity_) {  // geometric regrowth like KeyStore (core.hpp:134-142)
+            capacity_ *= 2;
+            detail::check(lv_reserve(ctx_.get(), (int64_t)capacity_, nullptr), "lv_reserve");
+        }
+        detail::check(lv_push_key(ctx_.get(), k.data(), v.data(), LV_F32, LV_HOST, nullptr), "lv_push_key");
+    }
+
+    // Folds pending keys into the index; false (no-op) when nothing is pending.
+    bool flush_buffer() { return detail::check(lv_flush(ctx_.get(), nullptr), "lv_flush") == LV_OK; }
+
+    CacheQueryResult query(const QueryRequest& req, FilterAlgo algo, bool strict_threshold = false) const {
+        if (req.q.size() != static_cast<size_t>(dim_)) throw std::invalid_argument("dot: length mismatch");
+        const int64_t words = lv_bitmap_words(ctx_.get());
+        detail::DevBuf bits(static_cast<size_t>(words) * 4), totals(4 * 8),
+            ws(lv_query_workspace_bytes(ctx_.get()));
+        Vector out(dim_, 0.0f);
+        int32_t counts[4] = {0, 0, 0, 0};
+        const float tau = req.tau;
+        lv_query_args a{};
+        a.q = req.q.data();
+        a.tau = &tau;
+        a.scale = req.effective_scale();
+        a.algo = static_cast<int>(algo);
+        a.strict = strict_threshold ? 1 : 0;
+        a.where = LV_HOST;
+        a.out = out.data();
+        a.counts = counts;
+        a.sel_bits = static_cast<uint32_t*>(bits.p);
+        a.totals = static_cast<uint64_t*>(totals.p);
+        a.workspace = ws.p;
+        detail::check(lv_query(ctx_.get(), &a), "lv_query");
+        const int64_t n_now = lv_n(ctx_.get()), indexed = lv_indexed_count(ctx_.get());
+        CacheQueryResult r;
+        r.selected = bits_to_ids(static_cast<const uint32_t*>(bits.p), n_now);
+        for (KeyId id : r.selected)
+            if (id < indexed) r.retrieved.push_back(id);
+        for (int64_t j = indexed; j < n_now; ++j) r.retrieved.push_back(static_cast<KeyId>(j));
+        uint64_t tot[4] = {0, 0, 0, 0};
+        detail::cuda_check(cudaMemcpy(tot, totals.p, sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        r.stats.groups_tested = static_cast<int64_t>(tot[0]);
+        r.stats.keys_scanned = counts[2];
+        r.stats.f_scan = n_now ? double(counts[2]) / double(n_now) : 1.0;
+        r.stats.gate_cost_equiv = 2.0 * double(tot[0]) / double(cfg_.r);
+        if (counts[3]) r.attention = AttentionResult{strict_threshold ? r.selected : r.retrieved, {}, std::move(out)};
+        return r;
+    }
+
+    int dim() const { return dim_; }
+    std::size_t n() const { return static_cast<size_t>(lv_n(ctx_.get())); }
+    std::size_t indexed_count() const { return static_cast<size_t>(lv_indexed_count(ctx_.get())); }
+    std::size_t pending_count() const { return static_cast<size_t>(lv_pending_count(ctx_.get())); }
+    std::vector<KeyId> pending_ids() const {
+        std::vector<KeyId> ids;
+        for (size_t j = indexed_count(); j < n(); ++j) ids.push_back(static_cast<KeyId>(j));
+        return ids;
+    }
+    std::size_t flush_count() const { return static_cast<size_t>(lv_flush_count(ctx_.get())); }
+    std::size_t buffer_capacity() const { return buffer_capacity_; }
+    // host copy of the stored rows (keys: values = false)
+    std::vector<Scalar> rows(bool values) const {
+        std::vector<Scalar> out(n() * dim_);
+        if (!out.empty())
+            detail::check(lv_read_rows(ctx_.get(), 0, 0, (int64_t)n(), values ? 1 : 0, out.data()), "lv_read_rows");
+        return out;
+    }
+    lv_ctx* handle() const { return ctx_.get(); }
+
+    // device bitmap [words] -> ascending ids < limit (device compaction kernel)
+    std::vector<KeyId> bits_to_ids(const uint32_t* dev_bits, int64_t limit) const {
+        if (limit <= 0) return {};
+        detail::DevBuf ids(static_cast<size_t>(limit) * 4), cnt(4);
+        detail::check(lv_bitmap_to_ids(dev_bits, lv_bitmap_words(ctx_.get()), 1, limit, static_cast<uint32_t*>(ids.p),
+                                       limit, static_cast<int32_t*>(cnt.p), nullptr),
+                      "lv_bitmap_to_ids");
+        int32_t c = 0;
+        detail::cuda_check(cudaMemcpy(&c, cnt.p, 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+        std::vector<KeyId> out(static_cast<size_t>(c));
+        if (c) detail::cuda_check(cudaMemcpy(out.data(), ids.p, 4 * static_cast<size_t>(c), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        return out;
+    }
+
+  private:
+    void create(std::size_t capacity) {
+        capacity_ = capacity;
+        lv_config c{};
+        c.d = dim_;
+        c.n_kv_heads = 1;
+        c.group_size = 1;
+        c.batch = 1;
+        c.dtype = LV_F32;
+        c.S = static_cast<int>(cfg_.S);
+        c.r = static_cast<int>(cfg_.r);
+        c.grouping = static_cast<int>(cfg_.grouping);
+        c.enclosure = static_cast<int>(cfg_.enclosing);
+        c.rng_seed = cfg_.rng_seed;
+        c.buffer_capacity = static_cast<int64_t>(buffer_capacity_);
+        c.capacity = static_cast<int64_t>(capacity);
+        lv_ctx* h = nullptr;
+        detail::check(lv_create(&c, &h), "lv_create");
+        ctx_.reset(h);
+    }
+
+    int dim_;
+    BuildConfig cfg_;
+    std::size_t buffer_capacity_;
+    std::size_t capacity_ = 0;
+    std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
+};
+
+// query.hpp:44-45: ids j < limit with dot(q, k_j) >= tau (normative dot, on the device).
+inline std::vector<KeyId> brute_force_range(const LouverCache& cache, ConstVecRef q, Scalar tau, std::size_t limit) {
+    if (limit > cache.n()) throw std::invalid_argument("brute_force_range: limit > n");
+    if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    if (limit == 0) return {};
+    detail::DevBuf bits(static_cast<size_t>(lv_bitmap_words(cache.handle())) * 4);
+    detail::check(lv_brute_force_range(cache.handle(), q.data(), &tau, (int64_t)limit, LV_HOST,
+                                       static_cast<uint32_t*>(bits.p), nullptr),
+                  "lv_brute_force_range");
+    return cache.bits_to_ids(static_cast<const uint32_t*>(bits.p), (int64_t)limit);
+}
+
+// query.hpp:69-72: softmax over sort∪unique(selected ∪ buffer); nullopt when empty.
+inline std::optional<AttentionResult> sparse_attention(const LouverCache& cache, std::span<const KeyId> buffer_ids,
+                                                       std::span<const KeyId> selected_ids, ConstVecRef q,
+                                                       Scalar scale) {
+    if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    std::vector<KeyId> tokens(selected_ids.begin(), selected_ids.end());
+    tokens.insert(tokens.end(), buffer_ids.begin(), buffer_ids.end());
+    std::sort(tokens.begin(), tokens.end());
+    tokens.erase(std::unique(tokens.begin(), tokens.end()), tokens.end());
+    AttentionResult r;
+    r.output.assign(cache.dim(), 0.0f);
+    r.weights.assign(tokens.size() ? tokens.size() : 1, 0.0f);
+    int64_t ntok = 0;
+    const int rc = detail::check(
+        lv_sparse_attention(cache.handle(), 0, buffer_ids.empty() ? nullptr : buffer_ids.data(), (int64_t)buffer_ids.size(),
+                            selected_ids.empty() ? nullptr : selected_ids.data(), (int64_t)selected_ids.size(),
+                            q.data(), scale, LV_HOST, r.output.data(), r.weights.data(), &ntok, nullptr),
+        "sparse_attention");
+    if (rc == LV_EMPTY) return std::nullopt;
+    r.weights.resize(static_cast<size_t>(ntok));
+    r.selected_ids = std::move(tokens);
+    return r;
+}
+
+// One decode layer: batch x H_kv slots (GQA group G), fp32 or bf16 KV in HBM.
+// query_device() is the hot path: device q [batch][H_q][d], tau [batch][H_q],
+// out [batch][H_q][d] (or partial [batch][H_q][d+2] for sequence sharding),
+// enqueue-only on `stream`.
+class LouverLayer {
+  public:
+    LouverLayer(int d, int n_kv_heads, int group_size, int batch, std::int64_t capacity, BuildConfig cfg,
+                std::size_t buffer_capacity, int dtype = LV_BF16) {
+        cfg.validate(d);
+        lv_config c{};
+        c.d = d;
+        c.n_kv_heads = n_kv_heads;
+        c.group_size = group_size;
+        c.batch = batch;
+        c.dtype = dtype;
+        c.S = static_cast<int>(cfg.S);
+        c.r = static_cast<int>(cfg.r);
+        c.grouping = static_cast<int>(cfg.grouping);
+        c.enclosure = static_cast<int>(cfg.enclosing);
+        c.rng_seed = cfg.rng_seed;
+        c.buffer_capacity = static_cast<int64_t>(buffer_capacity);
+        c.capacity = capacity;
+        lv_ctx* h = nullptr;
+        detail::check(lv_create(&c, &h), "lv_create");
+        ctx_.reset(h);
+    }
+    // K, V: [batch][H_kv][n][d], src_dtype LV_F32 / LV_BF16, host or device
+    void build(const void* K, const void* V, std::int64_t n, int src_dtype, int where, cudaStream_t st = nullptr) {
+        detail::check(lv_build(ctx_.get(), K, V, n, src_dtype, where, st), "lv_build");
+    }
+    // one new key per slot: k, v [batch][H_kv][d]
+    void push_key(const void* k, const void* v, int src_dtype, int where, cudaStream_t st = nullptr) {
+        detail::check(lv_push_key(ctx_.get(), k, v, src_dtype, where, st), "lv_push_key");
+    }
+    bool flush_buffer(cudaStream_t st = nullptr) { return detail::check(lv_flush(ctx_.get(), st), "lv_flush") == LV_OK; }
+    void query_device(const float* q, const float* tau, float* out, cudaStream_t st, float* partial = nullptr,
+                      int32_t* counts = nullptr, bool strict = false, float scale = 0.0f, void* workspace = nullptr) const {
+        lv_query_args a{};
+        a.q = q;
+        a.tau = tau;
+        a.scale = scale;
+        a.algo = LV_ALGO_TA;
+        a.strict = strict ? 1 : 0;
+        a.where = LV_DEVICE;
+        a.out = out;
+        a.partial = partial;
+        a.counts = counts;
+        a.workspace = workspace;
+        a.stream = st;
+        detail::check(lv_query(ctx_.get(), &a), "lv_query");
+    }
+    std::size_t workspace_bytes() const { return lv_query_workspace_bytes(ctx_.get()); }
+    std::int64_t n() const { return lv_n(ctx_.get()); }
+    lv_ctx* handle() const { return ctx_.get(); }
+
+  private:
+    std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
+};
+
+// Log-sum-exp merge of P sequence-shard partials [P][rows][d+2] -> out [rows][d].
+inline void lse_merge(const float* partials, int P, std::int64_t rows, int d, float* out, cudaStream_t st) {
+    detail::check(lv_lse_merge(partials, P, rows, d, out, st), "lv_lse_merge");
+}
+
+}  // namespace louver_b200

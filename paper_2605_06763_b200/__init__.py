@@ -6,6 +6,7 @@ over exactly that set, on sm_100a kernels behind the C ABI in
 include/louver_b200.h. See DESIGN.md.
 """
 from ._capi import LouverError, LIB_PATH, SYNTH_PATH  # noqa: F401
+from .sharding import ShardedLayer, gather_partials, insert_owner, shard_range  # noqa: F401
 from .louver import (  # noqa: F401
     AttentionResult,
     BuildConfig,
@@ -23,4 +24,5 @@ from .louver import (  # noqa: F401
 __all__ = [
     "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
     "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
+    "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
 ]

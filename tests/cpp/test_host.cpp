@@ -1,0 +1,213 @@
+// C++ host-layer parity test: include/louver_b200.hpp (the reference-shaped API)
+// against the CPU oracle (oracle/louver_oracle.h, test infrastructure) on seeded
+// synthetic streams with the reference laws (io.cpp:89-206).
+//
+// Mirrors the reference's own C++ tests: test_cache.cpp:102-144 (query vs
+// brute force, strict toggle, flush-at-B), test_query.cpp:178-196 (attention
+// known answers / nullopt), and test_core.cpp error behaviour.
+// usage: test_host [--compile-only]
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "louver_b200.hpp"
+#include "louver_oracle.h"
+
+using namespace louver_b200;
+
+static int failures = 0;
+#define EXPECT(cond, ...)                                   \
+    do {                                                    \
+        if (!(cond)) {                                      \
+            ++failures;                                     \
+            std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+            std::printf(__VA_ARGS__);                       \
+            std::printf("\n");                              \
+        }                                                   \
+    } while (0)
+
+static float bf16_round(float x) {  // round to nearest even, as the device conversion
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+    std::memcpy(&x, &u, 4);
+    return x;
+}
+
+static std::vector<uint32_t> oracle_range(const std::vector<float>& K, int64_t n, int d, const float* q, float tau) {
+    std::vector<uint32_t> ids(static_cast<size_t>(n ? n : 1));
+    int64_t cnt = 0;
+    lvo_brute_force_range(K.data(), n, d, q, tau, n, ids.data(), n, &cnt);
+    ids.resize(static_cast<size_t>(cnt));
+    return ids;
+}
+
+static double rel_err(const float* a, const float* b, int d) {
+    double num = 0, den = 0;
+    for (int i = 0; i < d; ++i) {
+        num += (double(a[i]) - b[i]) * (double(a[i]) - b[i]);
+        den += double(b[i]) * b[i];
+    }
+    return std::sqrt(num) / std::max(std::sqrt(den), 1e-30);
+}
+
+static void test_cache_fp32() {
+    const int d = 64;
+    const int64_t n0 = 3000, extra = 200;
+    std::vector<float> K((n0 + extra) * d), V((n0 + extra) * d), Q(4 * d);
+    lv_synth_keys(n0 + extra, d, 11, K.data());
+    lv_synth_keys(n0 + extra, d, 12, V.data());
+    lv_synth_queries(4, d, 13, Q.data());
+    KeyStore store(std::vector<float>(K.begin(), K.begin() + n0 * d), std::vector<float>(V.begin(), V.begin() + n0 * d), d);
+    BuildConfig cfg;
+    cfg.S = 4;
+    cfg.r = 16;
+    LouverCache cache(store, cfg, 64);
+    EXPECT(cache.n() == (size_t)n0 && cache.indexed_count() == (size_t)n0, "adopt indexes everything");
+    EXPECT(!cache.flush_buffer(), "empty flush returns false (cache.cpp:14)");
+    for (int64_t j = n0; j < n0 + extra; ++j)
+        cache.push_key({K.data() + j * d, (size_t)d}, {V.data() + j * d, (size_t)d});
+    EXPECT(cache.flush_count() == (size_t)(extra / 64), "flush-at-B: %zu flushes", cache.flush_count());
+    EXPECT(cache.pending_count() == (size_t)(extra % 64), "pending %zu", cache.pending_count());
+    const int64_t n = n0 + extra;
+    for (int qi = 0; qi < 4; ++qi) {
+        const float* q = Q.data() + qi * d;
+        const float tau = lvo_kth_score(K.data(), n, d, q, (n + 19) / 20);
+        QueryRequest req;
+        req.q.assign(q, q + d);
+        req.tau = tau;
+        for (int strict = 0; strict < 2; ++strict) {
+            CacheQueryResult r = cache.query(req, FilterAlgo::Ta, strict != 0);
+            const auto want = oracle_range(K, n, d, q, tau);
+            EXPECT(r.selected == want, "q%d selected: %zu vs oracle %zu", qi, r.selected.size(), want.size());
+            std::vector<uint32_t> ret;
+            for (uint32_t id : want)
+                if (id < cache.indexed_count()) ret.push_back(id);
+            for (size_t j = cache.indexed_count(); j < (size_t)n; ++j) ret.push_back((uint32_t)j);
+            EXPECT(r.retrieved == ret, "q%d retrieved", qi);
+            const auto& att = strict ? r.selected : r.retrieved;
+            std::vector<float> o(d);
+            int64_t ntok = 0;
+            const int rc = lvo_sparse_attention(K.data(), V.data(), n, d, nullptr, 0, att.data(), (int64_t)att.size(), q,
+                                                req.effective_scale(), o.data(), nullptr, &ntok);
+            EXPECT((rc == LVO_EMPTY) == !r.attention.has_value(), "q%d attention presence", qi);
+            if (r.attention) EXPECT(rel_err(r.attention->output.data(), o.data(), d) <= 1e-4, "q%d attention", qi);
+        }
+        const auto bf = brute_force_range(cache, {q, (size_t)d}, tau, (size_t)n);
+        EXPECT(bf == oracle_range(K, n, d, q, tau), "brute_force_range q%d", qi);
+    }
+    // sparse_attention: nullopt on an empty set, weights sum to 1 otherwise (query.cpp:338-371)
+    EXPECT(!sparse_attention(cache, {}, {}, {Q.data(), (size_t)d}, 0.125f).has_value(), "empty -> nullopt");
+    std::vector<KeyId> sel = {5, 1, 5, 900};
+    std::vector<KeyId> buf = {3100};
+    auto a = sparse_attention(cache, buf, sel, {Q.data(), (size_t)d}, 0.125f);
+    EXPECT(a && a->selected_ids == std::vector<KeyId>({1, 5, 900, 3100}), "sort-unique token set");
+    if (a) {
+        double s = 0;
+        for (float w : a->weights) s += w;
+        EXPECT(std::fabs(s - 1.0) < 1e-5, "weights sum %f", s);
+    }
+    // reference error behaviour
+    bool threw = false;
+    try {
+        cache.push_key({K.data(), (size_t)(d - 1)}, {V.data(), (size_t)d});
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "dimension mismatch -> std::invalid_argument");
+    threw = false;
+    try {
+        QueryRequest bad;
+        bad.q.assign(d + 1, 0.0f);
+        cache.query(bad, FilterAlgo::Ta);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "query length mismatch -> std::invalid_argument");
+    threw = false;
+    try {
+        BuildConfig c0;
+        c0.S = 0;
+        LouverCache bad(d, c0, 8);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "BuildConfig::validate -> std::invalid_argument");
+}
+
+static void test_layer_bf16() {
+    const int d = 128, H = 2, G = 4, B = 1;
+    const int64_t n = 4096;
+    std::vector<float> K(H * n * d), V(H * n * d), Q(H * G * d);
+    for (int h = 0; h < H; ++h) {
+        lv_synth_keys(n, d, 100 + h, K.data() + h * n * d);
+        lv_synth_keys(n, d, 200 + h, V.data() + h * n * d);
+    }
+    lv_synth_queries(H * G, d, 300, Q.data());
+    for (auto* v : {&K, &V, &Q})
+        for (float& x : *v) x = bf16_round(x);
+    std::vector<float> tau(H * G);
+    for (int hq = 0; hq < H * G; ++hq)
+        tau[hq] = lvo_kth_score(K.data() + (hq / G) * n * d, n, d, Q.data() + hq * d, n / 20);
+    BuildConfig cfg;
+    cfg.S = 1;
+    cfg.r = 16;
+    cfg.grouping = Grouping::Contiguous;
+    cfg.enclosing = EnclosureKind::Aabb;
+    LouverLayer layer(d, H, G, B, n, cfg, 128, LV_BF16);
+    layer.build(K.data(), V.data(), n, LV_F32, LV_HOST);
+    float *dq, *dt, *dout;
+    int32_t* dcnt;
+    cudaMalloc(&dq, Q.size() * 4);
+    cudaMalloc(&dt, tau.size() * 4);
+    cudaMalloc(&dout, Q.size() * 4);
+    cudaMalloc(&dcnt, H * G * 16);
+    cudaMemset(dcnt, 0, H * G * 16);
+    cudaMemcpy(dq, Q.data(), Q.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, tau.data(), tau.size() * 4, cudaMemcpyHostToDevice);
+    layer.query_device(dq, dt, dout, nullptr, nullptr, dcnt);
+    std::vector<float> out(Q.size());
+    std::vector<int32_t> cnt(H * G * 4);
+    cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cnt.data(), dcnt, cnt.size() * 4, cudaMemcpyDeviceToHost);
+    for (int hq = 0; hq < H * G; ++hq) {
+        const float* Kh = K.data() + (hq / G) * n * d;
+        const float* Vh = V.data() + (hq / G) * n * d;
+        std::vector<uint32_t> ids(n);
+        int64_t c = 0;
+        lvo_brute_force_range(Kh, n, d, Q.data() + hq * d, tau[hq], n, ids.data(), n, &c);
+        EXPECT(cnt[hq * 4 + 0] == c, "head %d selected count %d vs oracle %lld", hq, cnt[hq * 4], (long long)c);
+        std::vector<float> o(d);
+        int64_t ntok = 0;
+        lvo_sparse_attention(Kh, Vh, n, d, nullptr, 0, ids.data(), c, Q.data() + hq * d,
+                             (float)(1.0 / std::sqrt((double)d)), o.data(), nullptr, &ntok);
+        EXPECT(rel_err(out.data() + hq * d, o.data(), d) <= 1e-4, "head %d attention rel err %g", hq,
+               rel_err(out.data() + hq * d, o.data(), d));
+    }
+    cudaFree(dq);
+    cudaFree(dt);
+    cudaFree(dout);
+    cudaFree(dcnt);
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && std::strcmp(argv[1], "--compile-only") == 0) {
+        std::printf("%s\n", lv_build_info());
+        return 0;
+    }
+    try {
+        test_cache_fp32();
+        test_layer_bf16();
+    } catch (const std::exception& e) {
+        std::printf("FAIL exception: %s\n", e.what());
+        return 2;
+    }
+    if (failures) {
+        std::printf("%d failure(s)\n", failures);
+        return 1;
+    }
+    std::printf("OK\n");
+    return 0;
+}

@@ -75,24 +75,24 @@ struct CtxDeleter {
 };
 }  // namespace detail
 
-// index.hpp:13-20
-enum class Grouping { Contiguous = 0, Interleaved = 1, Random = 2, PcaTree = 3 };
-enum class EnclosureKind { Ball = 0, Aabb = 1, SpanBall = 2 };
+// types.hpp:16-27
+enum class GroupingStrategy : std::uint32_t { Contiguous = 0, Interleaved = 1, Random = 2, PcaTree = 3 };
+enum class EnclosureKind : std::uint32_t { Ball = 0, Aabb = 1, SpanBall = 2 };
 
 // index.hpp:10-22. On the device keys are grouped into contiguous cells of r keys
 // (r rounded up to a power of two, <= 64) with AABB summaries; S, grouping and
 // enclosing are validated like the reference and change pruning, never results.
 struct BuildConfig {
-    std::size_t S = 4;
-    std::size_t r = 4;
-    Grouping grouping = Grouping::PcaTree;
+    int S = 4;
+    int r = 4;
+    GroupingStrategy grouping = GroupingStrategy::PcaTree;
     EnclosureKind enclosing = EnclosureKind::Ball;
     std::uint64_t rng_seed = 0;
 
     void validate(int d) const {
         if (S < 1) throw std::invalid_argument("BuildConfig: S >= 1 required");
         if (r < 1) throw std::invalid_argument("BuildConfig: r >= 1 required");
-        if (S > static_cast<std::size_t>(d)) throw std::invalid_argument("BuildConfig: S <= d required");
+        if (S > d) throw std::invalid_argument("BuildConfig: S <= d required");
     }
 };
 

@@ -154,7 +154,7 @@ static void test_layer_bf16() {
     BuildConfig cfg;
     cfg.S = 1;
     cfg.r = 16;
-    cfg.grouping = Grouping::Contiguous;
+    cfg.grouping = GroupingStrategy::Contiguous;
     cfg.enclosing = EnclosureKind::Aabb;
     LouverLayer layer(d, H, G, B, n, cfg, 128, LV_BF16);
     layer.build(K.data(), V.data(), n, LV_F32, LV_HOST);

@@ -8,22 +8,28 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, in
     using Ge = C9<DP, G>;
     static int smem_set = 0;
     static int occ = 0;
-    const int ngrp = (vp.tiles + 31) / 32;
-    const int smem = Ge::smem(ngrp);
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(louver_layer_v9<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, louver_layer_v9<DP, G>, Ge::NTHR, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) return cudaErrorInvalidConfiguration;
-        smem_set = smem;
+    // one wave, CTAs of a slot's team side by side; CTA b lists the survivors of
+    // cells b, b + nb, ... so its list holds at most ceil(cap_cells / nb) cells
+    const long long cap_cells = vp.p.cap_cells;
+    int nb = vp.nb, smem = 0;
+    for (int it = 0; it < 8; ++it) {
+        smem = Ge::smem((int)((cap_cells + nb - 1) / nb));
+        if (smem > smem_set) {
+            cudaError_t e =
+                cudaFuncSetAttribute(louver_layer_v9<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, louver_layer_v9<DP, G>, Ge::NTHR, smem);
+            if (e != cudaSuccess) return e;
+            if (occ < 1) return cudaErrorInvalidConfiguration;
+            smem_set = smem;
+        }
+        int nb2 = occ * sms / slots;
+        if (nb2 > vp.nb) nb2 = vp.nb;  // workspace holds vp.nb partials per slot
+        if (nb2 < 1) nb2 = 1;
+        if (nb2 >= nb) break;  // the list capacity for nb CTAs fits the resident wave
+        nb = nb2;              // fewer CTAs per slot: longer lists, recheck
     }
-    // every CTA of a slot's team must be resident (per-slot barrier): size the
-    // grid to one wave and let it loop over slots if there are more
     const int cap = occ * sms;
-    int nb = cap / slots;
-    if (nb > vp.nb) nb = vp.nb;  // workspace holds vp.nb partials per slot
-    if (nb < 1) nb = 1;
     int gy = cap / nb;
     if (gy > slots) gy = slots;
     vp.nb = nb;

@@ -81,6 +81,33 @@ __device__ __forceinline__ unsigned bf2(float lo, float hi) {
     return (unsigned)lvk2::bf_bits(lo) | ((unsigned)lvk2::bf_bits(hi) << 16);
 }
 
+// Ballot over pair lanes (lane = k G + g for row k of a 32/G-row block) ->
+// bit k set iff any head of row k is set.
+template <int G>
+__device__ __forceinline__ unsigned row_bits(unsigned b) {
+    if constexpr (G == 1) {
+        return b & 0xffffu;
+    } else if constexpr (G == 2) {
+        unsigned x = (b | (b >> 1)) & 0x55555555u;
+        x = (x | (x >> 1)) & 0x33333333u;
+        x = (x | (x >> 2)) & 0x0f0f0f0fu;
+        x = (x | (x >> 4)) & 0x00ff00ffu;
+        return (x | (x >> 8)) & 0x0000ffffu;
+    } else if constexpr (G == 4) {
+        unsigned x = b | (b >> 1);
+        x = (x | (x >> 2)) & 0x11111111u;
+        x = (x | (x >> 3)) & 0x03030303u;
+        x = (x | (x >> 6)) & 0x000f000fu;
+        return (x | (x >> 12)) & 0xffu;
+    } else {
+        unsigned x = b | (b >> 1);
+        x |= x >> 2;
+        x = (x | (x >> 4)) & 0x01010101u;
+        x = (x | (x >> 7)) & 0x00030003u;
+        return (x | (x >> 14)) & 0xfu;
+    }
+}
+
 template <int DP, int G>
 struct C9 {
     static constexpr int NT = (3 * G + 7) / 8;   // exact: n-tiles of [q0|q1|q2]
@@ -92,7 +119,6 @@ struct C9 {
     static constexpr int PPL = G >= 2 ? G / 2 : 1;
     static constexpr int MT = DP / 16;           // P.V m-tiles (16 dims each)
     static constexpr int CT = 8 * (NT > NTP ? NT : NTP);  // C tile row pitch (floats)
-    static constexpr int CL = 1024;              // surviving cells per list segment
     static constexpr int MINB = DP <= 128 ? 2 : 1;
     static constexpr int SZ_FRE = KS * NT * 32 * 8;
     static constexpr int SZ_FRP = 2 * KS * NTP * 32 * 8;
@@ -101,17 +127,15 @@ struct C9 {
     static constexpr int OFF_Q = OFF_FRP + SZ_FRP;                    // [G][DP+4] f32
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
     static constexpr int MISC = 5 * G + 8 * G + 32;
-    static constexpr int OFF_CL = (OFF_M + MISC * 4 + 15) / 16 * 16;  // [CL] cell ids
-    static constexpr int FIX = (OFF_CL + CL * 4 + 127) / 128 * 128;
+    static constexpr int FIX = (OFF_M + MISC * 4 + 127) / 128 * 128;
     static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
     static constexpr int BUDGET = MINB == 2 ? 112 * 1024 : 224 * 1024;
     static constexpr int NW0 = (BUDGET - FIX) / PERW;
     static constexpr int NW = NW0 > 8 ? 8 : NW0;
     static constexpr int NTHR = NW * 32;
     static constexpr int OFF_W = FIX;                                 // per-warp areas
-    static constexpr int DYN = OFF_W + NW * PERW;                     // then [ngrp] gsum, [ngrp] gpre
-    static constexpr int MCG = 64;                                    // cache masks in smem up to 64 groups
-    static int smem(int ngrp) { return DYN + ngrp * 8 + (ngrp <= MCG ? ngrp * 64 : 0); }
+    static constexpr int DYN = OFF_W + NW * PERW;                     // then the survivor list
+    static int smem(int list_cap) { return DYN + list_cap * 4; }     // survivor cell list
     static_assert(NW >= 2, "Louver v9: shared memory budget too small");
 };
 
@@ -132,8 +156,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     float* S_s = misc + 3 * G;         // [G]
     float* red = misc + 5 * G;         // [8 G]
     int* iscr = reinterpret_cast<int*>(misc + 13 * G);  // [32]
-    unsigned* clist = reinterpret_cast<unsigned*>(smem + Ge::OFF_CL);
-    int* gsum = reinterpret_cast<int*>(smem + Ge::DYN);
+    unsigned* slist = reinterpret_cast<unsigned*>(smem + Ge::DYN);  // this CTA's surviving cells
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int blk = blockIdx.x, nb = vp.nb;
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
@@ -163,25 +186,35 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
         const unsigned char* sumb =
             reinterpret_cast<const unsigned char*>(vp.sum + (size_t)slot * p.cap_cells * (2 * DP));
-        unsigned short* cmask = vp.cmask + (size_t)slot * vp.tiles;
 
-        // ---- phase A prologue: the first summary blocks depend on nothing
-        const int wg = blk * NW + warp, pstride = nb * NW;
-        auto p_issue = [&](int u, int bound) {  // sub-task u: tile wg + (u>>1) pstride, half u&1 ([hi] or [lo])
-            const int tile = wg + (u >> 1) * pstride;
-            if (tile < bound) {
-                const unsigned char* src = sumb + ((size_t)tile * 16 * (2 * DP) + (u & 1) * DP) * 2;
+        // ---- phase A prologue: the first summary blocks depend on nothing.
+        // CTA blk of the team probes the slot's cells blk, blk + nb, blk + 2 nb, ... (a
+        // fine interleave: every CTA sees the same mix of the sequence, so the survivors
+        // split evenly with no team-wide exchange). CTA-local tile j = cells
+        // blk + (16 j + i) nb, i < 16; warp w takes tiles w, w + NW, ...
+        // Sub-task u of a warp: tile warp + (u >> 1) NW, half u & 1 ([hi] or [lo] rows).
+        if (tid == 0) {
+            iscr[2] = 0;  // survivors listed
+            iscr[3] = 0;  // tasks claimed
+        }
+        const long long cap_cells = p.cap_cells;
+        auto p_issue = [&](int u, long long bound) {
+            const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
+            if (c0 < bound) {
                 const unsigned dst = ring + (u % 3) * Ge::STAGE;
+                const size_t hoff = (size_t)(u & 1) * DP * 2;
 #pragma unroll
                 for (int k = 0; k < CPR / 2; ++k) {
                     const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
-                    cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), src + row * (2 * RB) + c * 16);
+                    long long cell = c0 + (long long)row * nb;
+                    cell = cell < cap_cells ? cell : cap_cells - 1;  // past the arena: any row, ignored
+                    cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), sumb + (size_t)cell * (4 * DP) + hoff + c * 16);
                 }
             }
             cpa_commit();
         };
-        p_issue(0, vp.tiles);
-        p_issue(1, vp.tiles);
+        p_issue(0, cap_cells);
+        p_issue(1, cap_cells);
 
         // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip)
         const long long n = __ldcg(&p.ctr->n);
@@ -272,7 +305,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(1)
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
-        const int ntile = (int)((ncells + 15) >> 4);
 
         // ---- phase A: probe
         {
@@ -281,9 +313,9 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             for (int g = 0; g < G; ++g) taup[g] = taup_s[g];
             float acc[NTP][4];
             for (int u = 0;; ++u) {
-                const int tile = wg + (u >> 1) * pstride;
-                if (tile >= ntile) break;
-                p_issue(u + 2, ntile);
+                const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
+                if (c0 >= ncells) break;
+                p_issue(u + 2, ncells);
                 cpa_wait<2>();
                 __syncwarp();
                 const int half = u & 1;
@@ -313,7 +345,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     __syncwarp();
                     unsigned gm = 0;
                     int scan = 0;
-                    const long long cell = ((long long)tile << 4) + lane;
+                    const long long cell = c0 + (long long)lane * nb;
                     if (lane < 16 && cell < ncells) {
                         const long long cs = cell << rl, ce = cs + r;
                         if (ce > indexed) {
@@ -326,7 +358,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         scan = (int)((ce < n ? ce : n) - cs);
                     }
                     const unsigned m = __ballot_sync(0xffffffffu, gm != 0) & 0xffffu;
-                    if (lane == 0) cmask[tile] = (unsigned short)m;
+                    if (m) {  // append the survivors to the CTA's list
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(iscr + 2, __popc(m));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (gm) slist[base + __popc(m & ((1u << lane) - 1u))] = (unsigned)cell;
+                    }
                     if (p.totals) {
                         const int tested = __popc(__ballot_sync(0xffffffffu, lane < 16 && cell < ncells));
                         if (lane == 0) {
@@ -349,47 +386,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         }
         LV9_TRACE(2)
 
-        // ---- per-slot barrier: every CTA of the team has published its masks
-        int* bar = vp.gtickets + (size_t)slot * vp.ngroups;
-        __syncthreads();  // the team's mask writes are ordered before the release below
-        if (tid == 0) {
-            red_release(bar, 1);
-            while (ld_acquire(bar) < nb) __nanosleep(32);
-        }
-        __syncthreads();
+        __syncthreads();  // the CTA's survivor list is complete
         LV9_TRACE(3)
-
-        // ---- surviving cells: per 32-tile group counts, exclusive prefix
-        const int ngrp = (ntile + 31) >> 5;
-        const int ngrp_cap = (vp.tiles + 31) >> 5;  // the dynamic smem layout
-        int* gpre = gsum + ngrp_cap;
-        unsigned short* mcache = ngrp_cap <= Ge::MCG ? reinterpret_cast<unsigned short*>(gpre + ngrp_cap) : nullptr;
-        for (int gi = warp; gi < ngrp; gi += NW) {
-            const int tile = gi * 32 + lane;
-            const unsigned m = tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
-            if (mcache) mcache[tile] = (unsigned short)m;
-            const int s = __reduce_add_sync(0xffffffffu, (unsigned)__popc(m));
-            if (lane == 0) gsum[gi] = s;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            int carry = 0;
-            for (int g0 = 0; g0 < ngrp; g0 += 32) {
-                const int v = g0 + lane < ngrp ? gsum[g0 + lane] : 0;
-                int incl = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                if (g0 + lane < ngrp) gpre[g0 + lane] = carry + incl - v;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) iscr[0] = carry;
-        }
-        __syncthreads();
-        const long long cs_total = iscr[0];
-        const long long c_lo = cs_total * blk / nb, c_hi = cs_total * (blk + 1) / nb;
+        const int nsurv = iscr[2];
+        if (trace && tid == 0) trace[11] = nsurv;
         LV9_TRACE(4)
 
         // ---- phase B: exact + attend
@@ -405,33 +405,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         int my_sel = 0, my_att = 0;
         unsigned long long t_keys = 0, t_vals = 0;
 
-        for (long long seg = c_lo; seg < c_hi; seg += Ge::CL) {
-            const long long seg_end = c_hi - seg < Ge::CL ? c_hi : seg + Ge::CL;
-            const int ncell = (int)(seg_end - seg);
-            for (int gi = warp; gi < ngrp; gi += NW) {  // cell ids of surviving cells [seg, seg_end)
-                const long long g_lo = gpre[gi];
-                if (g_lo >= seg_end || g_lo + gsum[gi] <= seg) continue;
-                const int tile = gi * 32 + lane;
-                unsigned m = mcache ? (unsigned)mcache[tile] : tile < ntile ? (unsigned)__ldcg(cmask + tile) : 0u;
-                const int cnt = __popc(m);
-                int incl = cnt;
-#pragma unroll
-                for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o2);
-                    if (lane >= o2) incl += t;
-                }
-                long long ci = g_lo + incl - cnt;
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    if (ci >= seg && ci < seg_end) clist[ci - seg] = (unsigned)(tile * 16 + b);
-                    ++ci;
-                }
-            }
-            __syncthreads();
-            const int ntask = ncell << tpc_l2;
+        {
+            // tasks = 16-key blocks of the listed cells, claimed through a shared counter
+            // one task ahead (balances warps whatever each task costs)
+            const int ntask = nsurv << tpc_l2;
             auto key0 = [&](int t) -> long long {
-                return ((long long)clist[t >> tpc_l2] << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
+                return ((long long)slist[t >> tpc_l2] << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
             };
             auto k_issue = [&](int t, int stage) {  // rows past n land as zeros
                 if (t < ntask) {
@@ -446,16 +425,23 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 cpa_commit();
             };
-            int t = warp, st = 0;
+            int ca = 0, cb = 0;
+            if (lane == 0) {
+                ca = atomicAdd(iscr + 3, 1);
+                cb = atomicAdd(iscr + 3, 1);
+            }
+            int t = __shfl_sync(0xffffffffu, ca, 0), st = 0;
             bool pend = false;
             unsigned pb[4] = {0u, 0u, 0u, 0u};  // B fragments of the pending task's P (hi b0 b1, lo b0 b1)
             k_issue(t, 0);
             cpa_commit();  // stands for V(t-1)
-            for (; t < ntask; t += NW) {
+            while (t < ntask) {
                 const int s1 = st == 2 ? 0 : st + 1;
                 const int s2 = st == 0 ? 2 : st - 1;  // stage of V(t-1)
                 const long long k0 = key0(t);
-                k_issue(t + NW, s1);
+                const int tn = __shfl_sync(0xffffffffu, cb, 0);
+                if (lane == 0 && tn < ntask) cb = atomicAdd(iscr + 3, 1);
+                k_issue(tn, s1);
                 cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
                 __syncwarp();
                 // -- scores: 16 keys x [q0|q1|q2] per head
@@ -534,14 +520,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     my_att += att;
                     s[j] = att ? scale * s[j] : -INFINITY;
                     mloc = fmaxf(mloc, s[j]);
-                    // row any-head flag: OR over the G lanes of the row, then one lane per row
-                    unsigned any = att;
-#pragma unroll
-                    for (int of = 1; of < G; of <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, of);
-                    const unsigned b = __ballot_sync(0xffffffffu, any && g_me == 0);
-                    // bits at lanes k*G -> rows j*(32/G) + k
-#pragma unroll
-                    for (int k = 0; k < 32 / G && k < 16; ++k) amask |= ((b >> (k * G)) & 1u) << (j * (32 / G) + k);
+                    amask |= row_bits<G>(__ballot_sync(0xffffffffu, att)) << (j * (32 / G));
                 }
                 if (lane == 0) t_keys += (k0 + 16 <= n) ? 16 : (n > k0 ? n - k0 : 0);
                 float alpha = 1.0f;
@@ -631,6 +610,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int e = 0; e < 4; ++e) pb[e] = nbf[e];
                 st = s1;
+                t = tn;
             }
             cpa_wait<0>();
             __syncwarp();
@@ -646,7 +626,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
             }
             __syncwarp();
-            __syncthreads();  // clist is rewritten by the next segment
         }
         LV9_TRACE(5)
 
@@ -813,10 +792,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 if (p.counts) p.counts[((size_t)slot * G + tid) * 4 + 3] = L[tid] > 0.0f ? 1 : 0;
             }
-            if (tid == 0) {
-                *ticket = 0;
-                *bar = 0;
-            }
+            if (tid == 0) *ticket = 0;
             LV9_TRACE(7)
         }
         __syncthreads();

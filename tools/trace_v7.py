@@ -46,6 +46,12 @@ def main():
     print(f"event time of traced query: {st.elapsed_time(en) * 1e3:.1f} us")
     tr = buf.cpu().numpy().astype(np.float64)
     t0 = tr[:, 0].min()
+    ns = tr[:, 11]
+    print(f"  survivors per CTA: min {ns.min():.0f} p10 {np.percentile(ns, 10):.0f} p50 {np.median(ns):.0f} "
+          f"p90 {np.percentile(ns, 90):.0f} max {ns.max():.0f}")
+    life = (tr[:, 5] - tr[:, 4]) / 1e3
+    print("  corr(survivors, task time) = %.2f; task-time per survivor p50 %.3f us" %
+          (np.corrcoef(ns, life)[0, 1], np.median(life / np.maximum(ns, 1))))
     fin = tr[tr[:, 7] > 0]
     for row in fin:
         r = (row - t0) / 1e3

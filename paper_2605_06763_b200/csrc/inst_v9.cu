@@ -11,9 +11,16 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, in
     // one wave, CTAs of a slot's team side by side; CTA b lists the survivors of
     // cells b, b + nb, ... so its list holds at most ceil(cap_cells / nb) cells
     const long long cap_cells = vp.p.cap_cells;
+    // CTA b of a slot's team owns cells b, b + nb, ...: its survivor list holds at most
+    // ceil(cap_cells / nb) u16 entries, in smem when that fits, else in global scratch
+    constexpr int kSmemMax = 227 * 1024;
     int nb = vp.nb, smem = 0;
+    bool glist = false;
     for (int it = 0; it < 8; ++it) {
-        smem = Ge::smem((int)((cap_cells + nb - 1) / nb));
+        const long long lc = (cap_cells + nb - 1) / nb;
+        if (lc > 65536) return cudaErrorInvalidValue;  // u16 interleave indices
+        glist = Ge::smem((int)lc) > kSmemMax;
+        smem = glist ? Ge::DYN : Ge::smem((int)lc);
         if (smem > smem_set) {
             cudaError_t e =
                 cudaFuncSetAttribute(louver_layer_v9<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -29,6 +36,8 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, in
         if (nb2 >= nb) break;  // the list capacity for nb CTAs fits the resident wave
         nb = nb2;              // fewer CTAs per slot: longer lists, recheck
     }
+    vp.list_cap = (int)((cap_cells + nb - 1) / nb);
+    if (!glist) vp.glist = nullptr;  // else: the caller's scratch of slots * (cap_cells + nb) entries
     const int cap = occ * sms;
     int gy = cap / nb;
     if (gy > slots) gy = slots;
@@ -45,9 +54,13 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, in
     cfg.blockDim = dim3(Ge::NTHR);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
+    // no grid-wide waiting remains (the merge ticket never blocks), so no cooperative
+    // launch is needed; the grid is still sized to one resident wave. Programmatic
+    // stream serialization lets the CTAs be dispatched while the previous kernel
+    // drains; the kernel's first instruction waits for that kernel's completion.
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G>, vp);

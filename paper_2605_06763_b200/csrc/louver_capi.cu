@@ -59,6 +59,7 @@ struct Workspace {
     float* tau = nullptr;      // [rows]
     float* part_out = nullptr; // [rows][DP+2]
     int* counts = nullptr;     // [rows][4]
+    unsigned short* glist = nullptr;  // [slots][cap_cells + nb] survivor lists (fused kernel, large contexts)
 };
 
 }  // namespace
@@ -113,7 +114,9 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
     unsigned char* gt = take(sizeof(int) * c->slots * ngr);
     unsigned char* stk = take(sizeof(int) * c->slots);
     unsigned char* cmk = take(sizeof(unsigned) * c->slots * (size_t)c->units);
+    unsigned char* gl = take(sizeof(unsigned short) * c->slots * ((size_t)c->cap_cells + c->nb));
     if (w) {
+        w->glist = reinterpret_cast<unsigned short*>(gl);
         w->gpart = reinterpret_cast<float*>(gp);
         w->gtickets = reinterpret_cast<int*>(gt);
         w->stickets = reinterpret_cast<int*>(stk);
@@ -308,6 +311,7 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         v5.ngroups = c->nb_groups;
         v5.gmax = nullptr;
         v5.p.tot_trace = c->trace;
+        v5.glist = w.glist;
         static const int k2 = [] { const char* e = getenv("LV_K2"); return e ? atoi(e) : 9; }();
         if (k2 == 7) e = lvk7::launch_query_v7(c->DP, c->G, v5, c->slots, st);
         else if (k2 == 8) e = lvk8::launch_query_v8(c->DP, c->G, v5, c->slots, st);

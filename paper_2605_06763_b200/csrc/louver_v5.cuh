@@ -52,6 +52,8 @@ struct V5Params {
     int ngroups;
     int* gmax;                 // optional [slot][G]: reset to the encoding of -inf by K1
     int slots;                 // v9: slots of the layer (the grid may loop over them)
+    unsigned short* glist;     // v9: survivor lists in global scratch when they outgrow smem (else null)
+    int list_cap;              // v9: entries per CTA list
 };
 
 // physical element of logical (k-step t, fragment element e in 0..3) for lane q:

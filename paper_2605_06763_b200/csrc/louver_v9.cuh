@@ -119,23 +119,23 @@ struct C9 {
     static constexpr int PPL = G >= 2 ? G / 2 : 1;
     static constexpr int MT = DP / 16;           // P.V m-tiles (16 dims each)
     static constexpr int CT = 8 * (NT > NTP ? NT : NTP);  // C tile row pitch (floats)
-    static constexpr int MINB = DP <= 128 ? 2 : 1;
+    static constexpr int MINB = 1;               // one CTA per SM: its warps share every task of the SM
     static constexpr int SZ_FRE = KS * NT * 32 * 8;
     static constexpr int SZ_FRP = 2 * KS * NTP * 32 * 8;
     static constexpr int OFF_FRE = 0;
     static constexpr int OFF_FRP = OFF_FRE + SZ_FRE;
     static constexpr int OFF_Q = OFF_FRP + SZ_FRP;                    // [G][DP+4] f32
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
-    static constexpr int MISC = 5 * G + 8 * G + 32;
+    static constexpr int MISC = 5 * G + 16 * G + 32;
     static constexpr int FIX = (OFF_M + MISC * 4 + 127) / 128 * 128;
     static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
-    static constexpr int BUDGET = MINB == 2 ? 112 * 1024 : 224 * 1024;
+    static constexpr int BUDGET = 223 * 1024;    // + the survivor list, within 227 KB
     static constexpr int NW0 = (BUDGET - FIX) / PERW;
-    static constexpr int NW = NW0 > 8 ? 8 : NW0;
+    static constexpr int NW = NW0 > 16 ? 16 : NW0;
     static constexpr int NTHR = NW * 32;
     static constexpr int OFF_W = FIX;                                 // per-warp areas
     static constexpr int DYN = OFF_W + NW * PERW;                     // then the survivor list
-    static int smem(int list_cap) { return DYN + list_cap * 4; }     // survivor cell list
+    static int smem(int list_cap) { return DYN + list_cap * 2; }     // survivor list (u16 interleave index)
     static_assert(NW >= 2, "Louver v9: shared memory budget too small");
 };
 
@@ -154,9 +154,11 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     float* taup_s = misc + G;          // [G] probe threshold tau - 2^-12 S
     float* marg_s = misc + 2 * G;      // [G] 2^-13 S
     float* S_s = misc + 3 * G;         // [G]
-    float* red = misc + 5 * G;         // [8 G]
-    int* iscr = reinterpret_cast<int*>(misc + 13 * G);  // [32]
-    unsigned* slist = reinterpret_cast<unsigned*>(smem + Ge::DYN);  // this CTA's surviving cells
+    float* red = misc + 5 * G;         // [16 G]
+    int* iscr = reinterpret_cast<int*>(misc + 21 * G);  // [32]
+    // this CTA's surviving cells as interleave indices k (cell = blk + k nb): in smem, or in
+    // global scratch when the list outgrows shared memory
+    unsigned short* slist_s = reinterpret_cast<unsigned short*>(smem + Ge::DYN);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int blk = blockIdx.x, nb = vp.nb;
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
@@ -170,6 +172,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     const int v_row = (lane & 7) + 8 * (lane >> 4), v_hi = (lane >> 3) & 1;
     const unsigned v_off = v_row * RB;
 
+    // programmatic dependent launch: dispatched early, but nothing is read before the
+    // preceding kernel in the stream has completed and flushed
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     long long* trace = nullptr;
 #define LV9_TRACE(i) \
     if (trace && tid == 0) trace[i] = lvk2::gtimer();
@@ -193,6 +199,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         // split evenly with no team-wide exchange). CTA-local tile j = cells
         // blk + (16 j + i) nb, i < 16; warp w takes tiles w, w + NW, ...
         // Sub-task u of a warp: tile warp + (u >> 1) NW, half u & 1 ([hi] or [lo] rows).
+        unsigned short* slist = vp.glist ? vp.glist + ((size_t)slot * nb + blk) * vp.list_cap : slist_s;
         if (tid == 0) {
             iscr[2] = 0;  // survivors listed
             iscr[3] = 0;  // tasks claimed
@@ -362,7 +369,9 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         int base = 0;
                         if (lane == 0) base = atomicAdd(iscr + 2, __popc(m));
                         base = __shfl_sync(0xffffffffu, base, 0);
-                        if (gm) slist[base + __popc(m & ((1u << lane) - 1u))] = (unsigned)cell;
+                        if (gm)
+                            slist[base + __popc(m & ((1u << lane) - 1u))] =
+                                (unsigned short)(16 * (warp + (u >> 1) * NW) + lane);
                     }
                     if (p.totals) {
                         const int tested = __popc(__ballot_sync(0xffffffffu, lane < 16 && cell < ncells));
@@ -389,7 +398,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         __syncthreads();  // the CTA's survivor list is complete
         LV9_TRACE(3)
         const int nsurv = iscr[2];
-        if (trace && tid == 0) trace[11] = nsurv;
         LV9_TRACE(4)
 
         // ---- phase B: exact + attend
@@ -410,7 +418,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             // one task ahead (balances warps whatever each task costs)
             const int ntask = nsurv << tpc_l2;
             auto key0 = [&](int t) -> long long {
-                return ((long long)slist[t >> tpc_l2] << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
+                const long long cell = blk + (long long)slist[t >> tpc_l2] * nb;
+                return (cell << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
             };
             auto k_issue = [&](int t, int stage) {  // rows past n land as zeros
                 if (t < ntask) {

@@ -45,6 +45,7 @@ def main():
     layer._ctx.lib.lv_debug_trace(layer._ctx.h, None)
     print(f"event time of traced query: {st.elapsed_time(en) * 1e3:.1f} us")
     tr = buf.cpu().numpy().astype(np.float64)
+    tr = tr[tr[:, 0] > 0]  # CTAs that ran
     t0 = tr[:, 0].min()
     ns = tr[:, 11]
     print(f"  survivors per CTA: min {ns.min():.0f} p10 {np.percentile(ns, 10):.0f} p50 {np.median(ns):.0f} "

@@ -421,16 +421,25 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 const long long cell = blk + (long long)slist[t >> tpc_l2] * nb;
                 return (cell << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
             };
+            // chunk k*32 + lane of a 16-row block: row k*RPI + lane/CPR, column chunk lane%CPR,
+            // so the source is base + 512 k + 16 lane and the swizzled destination repeats
+            // with period P in k: precompute the P per-lane destination offsets
+            constexpr int RPI = 32 / CPR, P = 8 / RPI;
+            unsigned doff[P];
+#pragma unroll
+            for (int kk = 0; kk < P; ++kk) {
+                const int row = kk * RPI + lane / CPR, c = lane % CPR;
+                doff[kk] = row * RB + ((c ^ (row & 7)) << 4);
+            }
             auto k_issue = [&](int t, int stage) {  // rows past n land as zeros
                 if (t < ntask) {
                     const long long kb = key0(t);
-                    const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks + (size_t)kb * DP);
+                    const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks + (size_t)kb * DP) + lane * 16;
                     const unsigned dst = ring + stage * Ge::STAGE;
+                    const long long lim = n - kb - lane / CPR;
 #pragma unroll
-                    for (int k = 0; k < CPR / 2; ++k) {
-                        const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
-                        cpa16z(dst + row * RB + ((c ^ (row & 7)) << 4), src + row * RB + c * 16, kb + row < n);
-                    }
+                    for (int k = 0; k < CPR / 2; ++k)
+                        cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, (long long)(k * RPI) < lim);
                 }
                 cpa_commit();
             };
@@ -572,11 +581,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 __syncwarp();  // K(t) and pbuf reads done
                 // -- V(t): attended rows into K(t)'s stage (same row positions)
-                if (amask) {
-                    constexpr int RPI = 32 / CPR;  // rows per warp instruction
+                if (amask) {  // RPI rows per warp instruction
                     unsigned mm = amask;
                     const unsigned dst = ring + st * Ge::STAGE;
-                    const int sub = lane / CPR, c = lane % CPR;
+                    const int cc = lane % CPR;
+                    const unsigned char* vsrc = reinterpret_cast<const unsigned char*>(Vs + (size_t)k0 * DP) + (lane % CPR) * 16;
+                    const int sub = lane / CPR;
                     while (mm) {
                         int rsel = -1;
 #pragma unroll
@@ -585,9 +595,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                             mm &= mm - 1;
                             if (k == sub) rsel = rr;
                         }
-                        if (rsel >= 0)
-                            cpa16(dst + rsel * RB + ((c ^ (rsel & 7)) << 4),
-                                  reinterpret_cast<const unsigned char*>(Vs + (size_t)(k0 + rsel) * DP) + c * 16);
+                        if (rsel >= 0) cpa16(dst + rsel * RB + ((cc ^ (rsel & 7)) << 4), vsrc + rsel * RB);
                     }
                 }
                 cpa_commit();

@@ -220,10 +220,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
             cpa_commit();
         };
-        p_issue(0, cap_cells);
-        p_issue(1, cap_cells);
-
-        // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip)
+        // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip,
+        // ahead of the summary prefetch so they do not queue behind it in the memory system)
         const long long n = __ldcg(&p.ctr->n);
         const long long indexed = __ldcg(&p.ctr->indexed);
         {
@@ -234,17 +232,22 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
             for (int k = 0; k < QPT; ++k) {
                 const int i = tid + k * NTHR;
-                xq[k] = i < G * DP ? __ldg(qsrc + i) : 0.0f;
-                xc[k] = i < G * DP ? __ldg(colmax + i % DP) : 0.0f;
+                xq[k] = i < G * DP ? __ldcg(qsrc + i) : 0.0f;
+                xc[k] = i < G * DP ? __ldcg(colmax + i % DP) : 0.0f;
             }
-            const float tau_r = tid < G ? __ldg(p.tau + (size_t)slot * G + tid) : 0.0f;
+            const float tau_r = tid < G ? __ldcg(p.tau + (size_t)slot * G + tid) : 0.0f;
             // zero the fragment arrays (columns past PARTS * G stay zero)
             for (int i = tid; i < (Ge::SZ_FRE + Ge::SZ_FRP) / 16; i += NTHR)
                 reinterpret_cast<uint4*>(smem + Ge::OFF_FRE)[i] = make_uint4(0u, 0u, 0u, 0u);
             float s[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) s[g] = 0.0f;
-            if (trace && tid == 0) trace[9] = lvk2::gtimer() + (long long)(xq[0] * 0.0f);
+            if (trace && tid == 0) {
+                asm volatile("" ::"f"(xq[0]));
+                trace[9] = lvk2::gtimer();
+                asm volatile("" ::"f"(xc[0]));
+                trace[12] = lvk2::gtimer();
+            }
 #pragma unroll
             for (int k = 0; k < QPT; ++k) {
                 const int i = tid + k * NTHR;
@@ -310,6 +313,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             __syncthreads();
         }
         LV9_TRACE(1)
+        // the summary prefetch starts only now: cp.async issue stalls the issuing warp once
+        // the memory system is saturated, so it must not sit in front of the setup
+        p_issue(0, cap_cells);
+        p_issue(1, cap_cells);
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
 
@@ -399,6 +406,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(3)
         const int nsurv = iscr[2];
         LV9_TRACE(4)
+        if (trace && tid == 0) trace[15] = nsurv;
 
         // ---- phase B: exact + attend
         const int g_me = lane % G;

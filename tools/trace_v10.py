@@ -1,8 +1,8 @@
-"""Per-CTA phase timing of the bf16 cell-stream kernel (louver_cells_v7) on one layer.
+"""Per-CTA phase timing of the bf16 layer kernel (v10) on one C2 layer.
 
-Phases: 0 start, 1 setup done, 2 griddepcontrol.wait returned (probe done),
-3 survivor prefix done, 4 first task begins, 5 last warp finished its tasks,
-6 CTA partial ready, 7 end (merge done).
+Stamps: 0 start, 1 setup done, 2 producer warp 0 done (probe), 3 consumer warp 0 starts
+its first task, 4 consumer warp 0 done, 5 every warp done, 6 CTA partial written,
+7 end (merge winners), 8 ticket won, 11 partial headers loaded, 15 tasks processed.
 """
 import os
 import sys
@@ -30,7 +30,7 @@ def main():
     out = torch.zeros((cfg["batch"], cfg["H_kv"] * G, cfg["d"]), device="cuda")
     slots = cfg["batch"] * cfg["H_kv"]
     nb = -(-2 * 148 // slots)
-    buf = torch.zeros((slots * nb, 16), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((slots * nb, 64), dtype=torch.int64, device="cuda")
     for _ in range(3):
         layer.query_device(q, t, out)
     torch.cuda.synchronize()
@@ -54,31 +54,23 @@ def main():
     tr = tr[tr[:, 0] > 0]  # CTAs that ran
     t0 = tr[:, 0].min()
     ns = tr[:, 15]
-    print(f"  survivors per CTA: min {ns.min():.0f} p10 {np.percentile(ns, 10):.0f} p50 {np.median(ns):.0f} "
-          f"p90 {np.percentile(ns, 90):.0f} max {ns.max():.0f}")
-    life = (tr[:, 5] - tr[:, 4]) / 1e3
-    print("  corr(survivors, task time) = %.2f; task-time per survivor p50 %.3f us" %
-          (np.corrcoef(ns, life)[0, 1], np.median(life / np.maximum(ns, 1))))
-    fin = tr[tr[:, 7] > 0]
-    for row in fin:
-        r = (row - t0) / 1e3
-        print(f"  final CTA: partial {r[6]:.2f} won {r[8]:.2f} headers {r[11]:.2f} "
-              f"chunk {r[13]:.2f} acc {r[14]:.2f} end {r[7]:.2f}")
-    for i, nm in ((9, "q loaded"), (12, "colmax"), (10, "S ready"), (1, "frags done")):
-        v = (tr[:, i] - t0) / 1e3
-        print(f"  setup {nm:10s} quantiles " + " ".join(f"{x:6.2f}" for x in np.percentile(v, [0, 50, 100])))
-    tr = tr[:, :8]
-    rel = (tr - t0) / 1e3
-    names = ["setup", "wait", "prefix", "cells", "tasks", "partial", "merge"]
-    print(f"CTAs {len(tr)}; start spread {rel[:, 0].max():.2f} us; last end {rel[:, 7].max():.2f} us")
-    for i in range(8):
-        v = rel[:, i][tr[:, i] > 0]
-        print(f"  t{i} abs quantiles " + " ".join(f"{x:7.2f}" for x in np.percentile(v, [0, 10, 50, 90, 100])))
-    for i in range(1, 8):
-        ok = (tr[:, i] > 0) & (tr[:, i - 1] > 0)
-        d = (tr[ok, i] - tr[ok, i - 1]) / 1e3
-        if d.size:
-            print(f"  {names[i - 1]:8s} mean {d.mean():7.3f}  p50 {np.median(d):7.3f}  p90 {np.percentile(d, 90):7.3f}  max {d.max():7.3f}")
+    print(f"  tasks per CTA: min {ns.min():.0f} p10 {np.percentile(ns, 10):.0f} p50 {np.median(ns):.0f} "
+          f"p90 {np.percentile(ns, 90):.0f} max {ns.max():.0f}  total {ns.sum():.0f}")
+    names = {9: "setup loads in", 10: "S reduced", 1: "setup done", 12: "prologue issued", 2: "probe done (pw0)", 3: "first task (cw0)", 4: "tasks done (cw0)",
+             5: "all warps done", 6: "CTA partial", 8: "ticket won", 11: "headers", 7: "merge end"}
+    print(f"CTAs {len(tr)}; last end {(tr[:, 7].max() - t0) / 1e3:.2f} us")
+    for i, nm in names.items():
+        v = (tr[:, i][tr[:, i] > 0] - t0) / 1e3
+        if v.size:
+            print(f"  {nm:18s} " + " ".join(f"{x:7.2f}" for x in np.percentile(v, [0, 10, 50, 90, 100])))
+    for lab, off in (("probe tile ready (pw0)", 16), ("task issue->wait (cw0)", 32), ("task K ready (cw0)", 48)):
+        print(f"  {lab}: p50 over CTAs per index")
+        row = []
+        for i in range(16):
+            v = tr[:, off + i]
+            v = (v[v > 0] - t0) / 1e3
+            row.append(f"{np.median(v):6.2f}" if v.size else "   -  ")
+        print("    " + " ".join(row))
 
 
 if __name__ == "__main__":

@@ -15,6 +15,8 @@
 #include "louver_b200.h"
 #include "louver_dispatch.h"
 #include "louver_v10.cuh"
+#include "louver_v11.cuh"
+#include "louver_v12.cuh"
 
 #include <cudaTypedefs.h>
 #include "louver_v2.cuh"
@@ -349,8 +351,13 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         v5.gmax = nullptr;
         v5.p.tot_trace = c->trace;
         v5.glist = w.glist;
+        // cells complete before the last insert enqueued ahead of this query: the insert kernel
+        // that may still be draining under PDL writes only the cell of key n - 1
+        v5.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
         static const int k2 = [] { const char* e = getenv("LV_K2"); return e ? atoi(e) : 9; }();
-        if (k2 != 10) {
+        if (k2 == 12) {
+            e = lvk12::launch_layer_v12(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
+        } else if (k2 != 10 && k2 != 11) {
             e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
         } else {
             lvk10::V10Params vp{};
@@ -364,7 +371,8 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
             vp.slots = c->slots;
             static const int dbg = [] { const char* e = getenv("LV_DBG"); return e ? atoi(e) : 0; }();
             vp.dbg = dbg;
-            e = lvk10::launch_layer_v10(c->DP, c->G, vp, c->sms, st, c->layer_geo);
+            e = k2 == 11 ? lvk11::launch_layer_v11(c->DP, c->G, vp, c->sms, st, c->layer_geo)
+                         : lvk10::launch_layer_v10(c->DP, c->G, vp, c->sms, st, c->layer_geo);
         }
     } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
         lvk2::V2Params vp{};

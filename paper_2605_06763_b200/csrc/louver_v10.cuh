@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
         };
         const unsigned sq0 = sq;
         int piss = 0;  // sub-blocks issued for this slot
-        int c0 = 0, c1 = 0, c2 = 0;  // lane 0: queue claims
+        int cl[8];  // lane 0: queue claims of tasks 0..5 (ring slots, see the consumer loop)
         // ---- setup: q, S_g, thresholds, B fragments
         const long long n = __ldcg(&p.ctr->n);
         const long long indexed = __ldcg(&p.ctr->indexed);
@@ -381,9 +381,8 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
                 p_issue(sq0 + v, tile, v & 1);
                 ++piss;
             }
-            c0 = atomicAdd(ctl + 1, 1);
-            c1 = atomicAdd(ctl + 1, 1);
-            c2 = atomicAdd(ctl + 1, 1);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) cl[k] = atomicAdd(ctl + 1, 1);
         }
         piss = __shfl_sync(0xffffffffu, piss, 0);
         if (trace && tid == 0) trace[12] = lvk2::gtimer();
@@ -430,7 +429,7 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
                 if (tile >= ntiles) break;
                 const unsigned st = (sq0 + v) % CST;
                 kwait(st);
-                if (trace && warp == 0 && lane == 0 && v < 16) trace[16 + v] = lvk2::gtimer();
+                
                 const unsigned tb = ring + st * STAGE;
                 if (h == 0) {
 #pragma unroll
@@ -535,17 +534,16 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
             const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
             const int qcap = vp.qcap;
             constexpr unsigned EXH = 0xffffffffu;
-            unsigned e0 = 0;  // lane 0: entry of claim c0 (0 = not seen yet)
-            // lane 0: block the warp until entry c0 is published or the queue is exhausted
-            auto spin_resolve = [&]() -> unsigned {
+            // lane 0: block the warp until entry c is published or the queue is exhausted
+            auto spin_resolve = [&](int c) -> unsigned {
                 for (;;) {
-                    if (c0 >= qcap) return EXH;
-                    const unsigned e = ld_relaxed(qe + c0);
+                    if (c >= qcap) return EXH;
+                    const unsigned e = ld_relaxed(qe + c);
                     const int pd = ld_acquire(ctl + 2);
                     if (e) return e;
                     if (pd >= total_prod) {
                         const int qr = ld_relaxed_i(ctl + 0);
-                        if (c0 >= qr) return EXH;
+                        if (c >= qr) return EXH;
                     }
                     __nanosleep(64);
                 }
@@ -557,7 +555,9 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
             bool pendA = false, pendB = false;
             float alphaB = 1.0f;  // alpha of task m-1 (frame m-2 -> m-1)
             int m = 0;
-            const unsigned sqc = sq;  // task j uses stage (sqc + j) % CST
+            // task j uses stage j % CST: start the consumer on a ring boundary (skipped stages
+            // carry no pending phase, their parity bits are untouched)
+            const unsigned sqc = (sq + CST - 1) / CST * CST;
             auto fold = [&](unsigned j, const unsigned (&pb)[4], bool any) {
                 const unsigned st = (sqc + j) % CST;
                 vwait(st);
@@ -584,51 +584,63 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
                     }
                 }
             };
-            for (;; ++m) {
-                // -- fold V(m-2) (frame m-2), then move o to frame m-1
-                if (m >= 2) {
-                    fold(m - 2, pbA, pendA);
-                    rescale(alphaB);
-                }
-                __syncwarp();
-                // -- keep two blocks ahead in flight
-                while (!exh && nis <= m + 2) {
-                    unsigned e = 0;
-                    if (lane == 0) {
-                        e = e0;
-                        if (e == 0) {
-                            if (nis <= m) {
-                                e = spin_resolve();
-                            } else {
-                                e0 = c0 < qcap ? ld_relaxed(qe + c0) : EXH;  // look again next round
-                            }
-                        }
-                    }
-                    e = __shfl_sync(0xffffffffu, e, 0);
-                    if (e == 0) break;
-                    if (e == EXH) {
-                        exh = true;
-                        break;
-                    }
-                    if (lane == 0) {
-                        const unsigned st = (sqc + nis) % CST;
-                        const long long k0 = (long long)(e - 1) << 4;
-                        kt[st] = k0;
-                        st_relaxed(qe + c0, 0u);  // consumed: the queue is left empty for the next launch
-                        fence_async();            // the stage was last touched by the generic proxy
-                        mbar_expect_tx(kbar + 8u * st, STAGE);
-                        const int y = (int)((long long)slot * p.cap + k0);
+            // Claims run 6 tasks ahead and their entries are read 4 tasks ahead, in rings of 8
+            // indexed by compile-time slots (the loop body is unrolled 8 times): a register
+            // whose atomic or load is still in flight is never copied, which would stall.
+            // lane 0: cl[] holds claimed queue indices, en[] their entries (0 = not published yet)
+            unsigned en[8];
+            auto ld_entry = [&](int c) { return c < qcap ? ld_relaxed(qe + c) : EXH; };
+            if (lane == 0) {
 #pragma unroll
-                        for (int pan = 0; pan < NPAN; ++pan)
-                            tma2d(ring + st * STAGE + pan * 2048, &vp.kmap, pan * 64, y, kbar + 8u * st);
-                        c0 = c1;
-                        c1 = c2;
-                        c2 = atomicAdd(ctl + 1, 1);
-                        e0 = c0 < qcap ? ld_relaxed(qe + c0) : EXH;
-                    }
-                    ++nis;
-                }
-                if (m >= nis) break;  // queue exhausted and every issued block processed
+                for (int k = 0; k < 4; ++k) en[k] = ld_entry(cl[k]);
+            }
+            auto issue_k = [&](unsigned e) {  // lane 0: K block of task nis
+                const unsigned st = (sqc + nis) % CST;
+                const long long k0 = (long long)(e - 1) << 4;
+                kt[st] = k0;
+                fence_async();  // the stage was last touched by the generic proxy
+                mbar_expect_tx(kbar + 8u * st, STAGE);
+                const int y = (int)((long long)slot * p.cap + k0);
+#pragma unroll
+                for (int pan = 0; pan < NPAN; ++pan) tma2d(ring + st * STAGE + pan * 2048, &vp.kmap, pan * 64, y, kbar + 8u * st);
+            };
+            // task m + OFF (ring slot JS) if it is the next one to issue; blocking when OFF == 0
+#define LV10_ISSUE(JS, OFF)                                                                   \
+    if (!exh && nis == m + (OFF)) {                                                             \
+        unsigned e = 0;                                                                         \
+        if (lane == 0) {                                                                        \
+            e = cl[JS] >= qcap ? EXH : en[JS];                                                  \
+            if (e == 0) {                                                                       \
+                if ((OFF) == 0) e = spin_resolve(cl[JS]);                                       \
+                else en[JS] = ld_relaxed(qe + cl[JS]); /* not published yet: look again later */ \
+            }                                                                                   \
+            if (e != 0 && e != EXH) {                                                           \
+                issue_k(e);                                                                     \
+                st_relaxed(qe + cl[JS], 0u); /* consumed: the queue stays empty between launches */ \
+                cl[((JS) + 6) % 8] = atomicAdd(ctl + 1, 1);                                     \
+                en[((JS) + 4) % 8] = ld_entry(cl[((JS) + 4) % 8]);                              \
+            }                                                                                   \
+        }                                                                                       \
+        e = __shfl_sync(0xffffffffu, e, 0);                                                     \
+        if (e == EXH) exh = true;                                                               \
+        else if (e != 0) ++nis;                                                                 \
+    }
+#define LV10_BODY(J)                                                  \
+    {                                                                   \
+        if (trace && warp == 0 && lane == 0 && m < 16) trace[16 + m] = lvk2::gtimer(); \
+        if (m >= 2) { /* fold V(m-2) (frame m-2), then move o to frame m-1 */ \
+            fold(m - 2, pbA, pendA);                                    \
+            rescale(alphaB);                                            \
+        }                                                               \
+        __syncwarp();                                                   \
+        LV10_ISSUE((J), 0)                                              \
+        LV10_ISSUE(((J) + 1) % 8, 1)                                    \
+        LV10_ISSUE(((J) + 2) % 8, 2)                                    \
+        if (m >= nis) break; /* exhausted, every issued block processed */ \
+        task();                                                         \
+        ++m;                                                            \
+    }
+            auto task = [&]() {
                 __syncwarp();
                 // -- task m: scores of 16 keys x [q0|q1|q2] per head
                 const unsigned st = (sqc + m) % CST;
@@ -788,7 +800,19 @@ __global__ void __launch_bounds__(C10<DP, G>::NTHR, 1) louver_layer_v10(const __
                 pendB = amask != 0;
                 // alpha of task m (frame m-1 -> m) applies once V(m-1) is folded
                 alphaB = alpha;
+            };
+            for (;;) {
+                LV10_BODY(0)
+                LV10_BODY(1)
+                LV10_BODY(2)
+                LV10_BODY(3)
+                LV10_BODY(4)
+                LV10_BODY(5)
+                LV10_BODY(6)
+                LV10_BODY(7)
             }
+#undef LV10_BODY
+#undef LV10_ISSUE
             // drain: the exit round already folded V(m-2); V(m-1) remains (m = tasks processed)
             if (m >= 1) fold(m - 1, pbB, pendB);
             sq = sqc + nis;

@@ -27,7 +27,7 @@
 
 #include "louver_v5.cuh"
 
-namespace lvk9 {
+namespace lvk12 {
 
 using lvk::QueryParams;
 using lvk5::V5Params;
@@ -109,7 +109,7 @@ __device__ __forceinline__ unsigned row_bits(unsigned b) {
 }
 
 template <int DP, int G>
-struct C9 {
+struct C12 {
     static constexpr int NT = (3 * G + 7) / 8;   // exact: n-tiles of [q0|q1|q2]
     static constexpr int NTP = (2 * G + 7) / 8;  // probe: n-tiles of [p0|p1]
     static constexpr int KS = DP / 16;
@@ -128,7 +128,8 @@ struct C9 {
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
     static constexpr int MISC = 5 * G + 16 * G + 32;
     static constexpr int FIX = (OFF_M + MISC * 4 + 127) / 128 * 128;
-    static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
+    static constexpr int CST = 4;                // ring stages per warp
+    static constexpr int PERW = CST * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
     static constexpr int BUDGET = 223 * 1024;    // + the survivor list, within 227 KB
     static constexpr int NW0 = (BUDGET - FIX) / PERW;
     static constexpr int NW = NW0 > 16 ? 16 : NW0;
@@ -136,12 +137,12 @@ struct C9 {
     static constexpr int OFF_W = FIX;                                 // per-warp areas
     static constexpr int DYN = OFF_W + NW * PERW;                     // then the survivor list
     static int smem(int list_cap) { return DYN + list_cap * 2; }     // survivor list (u16 interleave index)
-    static_assert(NW >= 2, "Louver v9: shared memory budget too small");
+    static_assert(NW >= 2, "Louver v12: shared memory budget too small");
 };
 
 template <int DP, int G>
-__global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ V5Params vp) {
-    using Ge = C9<DP, G>;
+__global__ void __launch_bounds__(C12<DP, G>::NTHR, C12<DP, G>::MINB) louver_layer_v12(const __grid_constant__ V5Params vp) {
+    using Ge = C12<DP, G>;
     constexpr int NW = Ge::NW, NTHR = Ge::NTHR, NT = Ge::NT, NTP = Ge::NTP, KS = Ge::KS, CPR = Ge::CPR,
                   RB = Ge::RB, PPL = Ge::PPL, MT = Ge::MT, CT = Ge::CT;
     const QueryParams& p = vp.p;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     const int blk = blockIdx.x, nb = vp.nb;
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
     const unsigned ring = lvk2::smem_u32(wbase);
-    float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
+    float* ct = reinterpret_cast<float*>(wbase + Ge::CST * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
     const int q4 = lane & 3;
     // per-lane ldmatrix offsets: A (rows = keys / cells) and V^T (trans)
@@ -172,23 +173,22 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     const int v_row = (lane & 7) + 8 * (lane >> 4), v_hi = (lane >> 3) & 1;
     const unsigned v_off = v_row * RB;
 
-    // programmatic dependent launch: dispatched early, while the preceding kernel in the
-    // stream drains; only immutable data (sealed cell summaries) is read before
-    // griddepcontrol.wait below
+    // programmatic dependent launch: dispatched early, but nothing is read before the
+    // preceding kernel in the stream has completed and flushed
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    bool waited = false;
     long long* trace = nullptr;
-#define LV9_TRACE(i) \
+#define LV12_TRACE(i) \
     if (trace && tid == 0) trace[i] = lvk2::gtimer();
 
     // zero the ring once: rows of a V stage that are not loaded meet P = 0
-    for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
+    for (int i = lane; i < Ge::CST * Ge::STAGE / 16; i += 32)
         *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
 
     for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
         trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 16 : nullptr;
-        LV9_TRACE(0)
+        LV12_TRACE(0)
         const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
         const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
         const unsigned char* sumb =
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         auto p_issue = [&](int u, long long bound) {
             const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
             if (c0 < bound) {
-                const unsigned dst = ring + (u % 3) * Ge::STAGE;
+                const unsigned dst = ring + (u % Ge::CST) * Ge::STAGE;
                 const size_t hoff = (size_t)(u & 1) * DP * 2;
 #pragma unroll
                 for (int k = 0; k < CPR / 2; ++k) {
@@ -221,21 +221,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
             cpa_commit();
         };
-        // The first summary tile of this warp is prefetched before the dependency wait when
-        // its cells were complete when the query was enqueued (vp.sealed): a complete
-        // cell's box never changes, so it cannot depend on the preceding kernel (an insert
-        // only writes the open cell). Its stream then overlaps the preceding kernel's tail.
-        bool pre = false;
-        if (!waited) {
-            const long long c0 = blk + (long long)16 * warp * nb;
-            pre = c0 >= cap_cells || c0 + 15LL * nb < vp.sealed;
-            if (pre) {
-                p_issue(0, cap_cells);
-                p_issue(1, cap_cells);
-            }
-            asm volatile("griddepcontrol.wait;\n" ::: "memory");
-            waited = true;
-        }
         // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip,
         // ahead of the summary prefetch so they do not queue behind it in the memory system)
         const long long n = __ldcg(&p.ctr->n);
@@ -293,7 +278,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 taup_s[tid] = __fsub_rd(tau, __fmul_ru(v, 2.44140625e-4f));  // 2^-12 S
                 marg_s[tid] = __fmul_ru(v, 1.220703125e-4f);                 // 2^-13 S
             }
-            LV9_TRACE(10)
+            LV12_TRACE(10)
             // each q element scatters its bf16 split parts straight into the B fragments:
             // element k of head g, part P sits in column P G + g; within a k-step of 16,
             // r = k % 16 -> lane quad (r & 7) / 2, half e = (r & 1) | (r >> 3) << 1
@@ -328,13 +313,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
             __syncthreads();
         }
-        LV9_TRACE(1)
+        LV12_TRACE(1)
         // the summary prefetch starts only now: cp.async issue stalls the issuing warp once
         // the memory system is saturated, so it must not sit in front of the setup
-        if (!pre) {
-            p_issue(0, cap_cells);
-            p_issue(1, cap_cells);
-        }
+        p_issue(0, cap_cells);
+        p_issue(1, cap_cells);
+        p_issue(2, cap_cells);
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
 
@@ -347,15 +331,15 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             for (int u = 0;; ++u) {
                 const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
                 if (c0 >= ncells) break;
-                p_issue(u + 2, ncells);
-                cpa_wait<2>();
+                p_issue(u + 3, ncells);
+                cpa_wait<3>();
                 __syncwarp();
                 const int half = u & 1;
                 if (half == 0) {
 #pragma unroll
                     for (int nt = 0; nt < NTP; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
                 }
-                const unsigned sb = ring + (u % 3) * Ge::STAGE + a_off;
+                const unsigned sb = ring + (u % Ge::CST) * Ge::STAGE + a_off;
                 const uint2* fh = frp + half * KS * NTP * 32;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
@@ -418,12 +402,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             cpa_wait<0>();
             __syncwarp();
         }
-        LV9_TRACE(2)
+        LV12_TRACE(2)
 
         __syncthreads();  // the CTA's survivor list is complete
-        LV9_TRACE(3)
+        LV12_TRACE(3)
         const int nsurv = iscr[2];
-        LV9_TRACE(4)
+        LV12_TRACE(4)
         if (trace && tid == 0) trace[15] = nsurv;
 
         // ---- phase B: exact + attend
@@ -469,25 +453,60 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 cpa_commit();
             };
-            int ca = 0, cb = 0;
+            // Pipeline per warp (iteration i, task t_i in stage i % 4): fold V(i-2) | issue
+            // K(i+2) into the stage it freed | score K(i), issue V(i) into K(i)'s stage.
+            // cp.async groups are committed in the order K(i+2), V(i) each iteration.
+            int ca = 0, cb = 0, cc = 0;
             if (lane == 0) {
                 ca = atomicAdd(iscr + 3, 1);
                 cb = atomicAdd(iscr + 3, 1);
+                cc = atomicAdd(iscr + 3, 1);
             }
             int t = __shfl_sync(0xffffffffu, ca, 0), st = 0;
-            bool pend = false;
-            unsigned pb[4] = {0u, 0u, 0u, 0u};  // B fragments of the pending task's P (hi b0 b1, lo b0 b1)
+            int tn1 = __shfl_sync(0xffffffffu, cb, 0);  // task of iteration i + 1
+            // tasks i-2 (A) and i-1 (B) await their V fold: P fragments, any rows, alpha
+            unsigned pbA[4] = {0u, 0u, 0u, 0u}, pbB[4] = {0u, 0u, 0u, 0u};
+            bool pendA = false, pendB = false;
+            float alphaB = 1.0f;  // alpha of task i-1 (frame i-2 -> i-1)
             k_issue(t, 0);
-            cpa_commit();  // stands for V(t-1)
+            cpa_commit();  // stands for V(-2)
+            k_issue(tn1, 1);
+            cpa_commit();  // stands for V(-1)
+            auto foldv = [&](int stage, const unsigned (&pbv)[4]) {
+                const unsigned vb = ring + stage * Ge::STAGE + v_off;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    unsigned a[4];
+                    ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
+                    mma16816(o[mt], a, pbv[0], pbv[1]);
+                    mma16816(o[mt], a, pbv[2], pbv[3]);
+                }
+            };
+            auto rescale = [&](float alpha) {
+                if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+                    const float a0 = __shfl_sync(0xffffffffu, alpha, (2 * q4) % G);
+                    const float a1 = __shfl_sync(0xffffffffu, alpha, (2 * q4 + 1) % G);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        o[mt][0] *= a0;
+                        o[mt][1] *= a1;
+                        o[mt][2] *= a0;
+                        o[mt][3] *= a1;
+                    }
+                }
+            };
             while (t < ntask) {
-                const int s1 = st == 2 ? 0 : st + 1;
-                const int s2 = st == 0 ? 2 : st - 1;  // stage of V(t-1)
+                const int s2 = (st + 2) & 3;  // stage of V(i-2), then of K(i+2)
                 const long long k0 = key0(t);
-                const int tn = __shfl_sync(0xffffffffu, cb, 0);
-                if (lane == 0 && tn < ntask) cb = atomicAdd(iscr + 3, 1);
-                k_issue(tn, s1);
-                cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
+                cpa_wait<2>();  // V(i-2) and K(i) landed (K(i+1), V(i-1) may pend)
                 __syncwarp();
+                // -- fold V(i-2) (frame i-2), then move o to frame i-1
+                if (pendA) foldv(s2, pbA);
+                rescale(alphaB);
+                __syncwarp();
+                const int tn2 = __shfl_sync(0xffffffffu, cc, 0);
+                if (lane == 0 && tn2 < ntask) cc = atomicAdd(iscr + 3, 1);
+                k_issue(tn2, s2);
                 // -- scores: 16 keys x [q0|q1|q2] per head
                 const unsigned sb = ring + st * Ge::STAGE;
                 {
@@ -625,52 +644,30 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     }
                 }
                 cpa_commit();
-                // -- fold V(t-1) (frame m_{t-1}), then move o to frame m_t
-                cpa_wait<2>();  // V(t-1) landed (K(t+1), V(t) may pend)
-                __syncwarp();
-                if (pend) {
-                    const unsigned vb = ring + s2 * Ge::STAGE + v_off;
+                // shift the fold pipeline
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        unsigned a[4];
-                        ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
-                        mma16816(o[mt], a, pb[0], pb[1]);
-                        mma16816(o[mt], a, pb[2], pb[3]);
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    pbA[e] = pbB[e];
+                    pbB[e] = nbf[e];
                 }
-                if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-                    const float a0 = __shfl_sync(0xffffffffu, alpha, (2 * q4) % G);
-                    const float a1 = __shfl_sync(0xffffffffu, alpha, (2 * q4 + 1) % G);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        o[mt][0] *= a0;
-                        o[mt][1] *= a1;
-                        o[mt][2] *= a0;
-                        o[mt][3] *= a1;
-                    }
-                }
-                pend = amask != 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) pb[e] = nbf[e];
-                st = s1;
-                t = tn;
+                pendA = pendB;
+                pendB = amask != 0;
+                const float alphaA = alphaB;
+                alphaB = alpha;
+                (void)alphaA;
+                st = (st + 1) & 3;
+                t = tn1;
+                tn1 = tn2;
             }
+            // drain: V(i-2) (frame i-2), alpha_{i-1}, V(i-1)
             cpa_wait<0>();
             __syncwarp();
-            if (pend) {  // the last task's V
-                const int s2 = st == 0 ? 2 : st - 1;
-                const unsigned vb = ring + s2 * Ge::STAGE + v_off;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    unsigned a[4];
-                    ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
-                    mma16816(o[mt], a, pb[0], pb[1]);
-                    mma16816(o[mt], a, pb[2], pb[3]);
-                }
-            }
+            if (pendA) foldv((st + 2) & 3, pbA);
+            rescale(alphaB);
+            if (pendB) foldv((st + 3) & 3, pbB);
             __syncwarp();
         }
-        LV9_TRACE(5)
+        LV12_TRACE(5)
 
         // ---- statistics: lanes with the same g = lane % G hold that head's counts
         if (p.counts) {
@@ -736,7 +733,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * Wd + g * (DP + 2) + 2 + c], s);
             part[g * (DP + 2) + 2 + c] = s;
         }
-        LV9_TRACE(6)
+        LV12_TRACE(6)
 
         // ---- phase C: the last CTA of the team merges the nb partials
         int* ticket = vp.stickets + slot;
@@ -744,7 +741,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         if (tid == 0) iscr[1] = atom_add_acq_rel(ticket, 1) == nb - 1;
         __syncthreads();
         if (iscr[1]) {
-            LV9_TRACE(8)
+            LV12_TRACE(8)
             const float* src = p.partial_ws + (size_t)slot * nb * Wd;
             // scratch over the rings: M[G], L[G], m/weights [nb][G], l [nb][G], then the o chunks
             float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);
@@ -776,7 +773,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 lsv[i] = __ldcg(h + 1);
             }
             __syncthreads();
-            LV9_TRACE(11)
+            LV12_TRACE(11)
             for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
                 float mm = -INFINITY;
                 for (int s2 = lane; s2 < nb; s2 += 32) mm = fmaxf(mm, wgt[s2 * G + g]);
@@ -803,7 +800,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (s0 > 0) chunk_issue(s0);
                 cpa_wait<0>();
                 __syncthreads();
-                LV9_TRACE(13)
+                LV12_TRACE(13)
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int i = tid + k * NTHR;
@@ -817,7 +814,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 __syncthreads();
             }
-            LV9_TRACE(14)
+            LV12_TRACE(14)
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 const int i = tid + k * NTHR;
@@ -836,17 +833,17 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (p.counts) p.counts[((size_t)slot * G + tid) * 4 + 3] = L[tid] > 0.0f ? 1 : 0;
             }
             if (tid == 0) *ticket = 0;
-            LV9_TRACE(7)
+            LV12_TRACE(7)
         }
         __syncthreads();
         // the ring was used as merge scratch: restore zeros for the next slot
-        for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
+        for (int i = lane; i < Ge::CST * Ge::STAGE / 16; i += 32)
             *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
     }
-#undef LV9_TRACE
+#undef LV12_TRACE
 }
 
-cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st, int* geo);
+cudaError_t launch_layer_v12(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st, int* geo);
 
-}  // namespace lvk9
+}  // namespace lvk12

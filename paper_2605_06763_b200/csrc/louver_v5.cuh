@@ -54,6 +54,7 @@ struct V5Params {
     int slots;                 // v9: slots of the layer (the grid may loop over them)
     unsigned short* glist;     // v9: survivor lists in global scratch when they outgrow smem (else null)
     int list_cap;              // v9: entries per CTA list
+    long long sealed;          // v9: cells complete when the query was enqueued (immutable summaries)
 };
 
 // physical element of logical (k-step t, fragment element e in 0..3) for lane q:

@@ -31,7 +31,7 @@ def main():
     slots = cfg["batch"] * cfg["H_kv"]
     nb = -(-2 * 148 // slots)
     buf = torch.zeros((slots * nb, 64), dtype=torch.int64, device="cuda")
-    for _ in range(3):
+    for _ in range(int(os.environ.get("WARM", "300"))):  # keep the clocks up
         layer.query_device(q, t, out)
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -56,14 +56,14 @@ def main():
     ns = tr[:, 15]
     print(f"  tasks per CTA: min {ns.min():.0f} p10 {np.percentile(ns, 10):.0f} p50 {np.median(ns):.0f} "
           f"p90 {np.percentile(ns, 90):.0f} max {ns.max():.0f}  total {ns.sum():.0f}")
-    names = {9: "setup loads in", 10: "S reduced", 1: "setup done", 12: "prologue issued", 2: "probe done (pw0)", 3: "first task (cw0)", 4: "tasks done (cw0)",
+    names = {9: "setup loads in", 10: "S reduced", 1: "setup done", 12: "prologue issued", 13: "loader probe issued", 14: "loader keys done", 2: "probe done (pw0)", 3: "first task (cw0)", 4: "tasks done (cw0)",
              5: "all warps done", 6: "CTA partial", 8: "ticket won", 11: "headers", 7: "merge end"}
     print(f"CTAs {len(tr)}; last end {(tr[:, 7].max() - t0) / 1e3:.2f} us")
     for i, nm in names.items():
         v = (tr[:, i][tr[:, i] > 0] - t0) / 1e3
         if v.size:
             print(f"  {nm:18s} " + " ".join(f"{x:7.2f}" for x in np.percentile(v, [0, 10, 50, 90, 100])))
-    for lab, off in (("probe tile ready (pw0)", 16), ("task issue->wait (cw0)", 32), ("task K ready (cw0)", 48)):
+    for lab, off in (("iteration start, before V fold (w0)", 16), ("task issue->wait (w0)", 32), ("task K ready (w0)", 48)):
         print(f"  {lab}: p50 over CTAs per index")
         row = []
         for i in range(16):

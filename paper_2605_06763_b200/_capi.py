@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblouver_b200.so")
+LIB_PATH = os.environ.get("LOUVER_B200_LIB") or os.path.join(_HERE, "liblouver_b200.so")  # env: A/B builds (tools only)
 SYNTH_PATH = os.path.join(_HERE, "liblouver_synth.so")
 
 LV_OK, LV_EMPTY, LV_EINVAL, LV_ERANGE, LV_ERUNTIME, LV_ENODEV = 0, 1, -1, -2, -3, -4

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     __syncwarp();
 
     for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
-        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 16 : nullptr;
+        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 32 : nullptr;
         LV9_TRACE(0)
         const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
         const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
             asm volatile("griddepcontrol.wait;\n" ::: "memory");
             waited = true;
+            LV9_TRACE(13)
         }
         // ---- setup: q, S_g, thresholds, B fragments (all inputs requested in one round trip,
         // ahead of the summary prefetch so they do not queue behind it in the memory system)
@@ -745,73 +746,57 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         __syncthreads();
         if (iscr[1]) {
             LV9_TRACE(8)
+            // all nb partials travel in one round trip: headers and o rows staged together
             const float* src = p.partial_ws + (size_t)slot * nb * Wd;
-            // scratch over the rings: M[G], L[G], m/weights [nb][G], l [nb][G], then the o chunks
-            float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);
+            float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);  // scratch over the rings
             float* L = M + G;
-            float* wgt = M + 2 * G;
-            float* lsv = wgt + nb * G;
-            const int hdr = (2 * G + 2 * nb * G + 3) / 4 * 4;
+            float* wgt = M + 2 * G;                        // [nb][G]
+            float* stg = wgt + ((nb * G + 3) / 4) * 4;     // [per_chunk][Wd]
             constexpr int EPT = (G * DP + NTHR - 1) / NTHR;
+            const int per_chunk = (NW * Ge::PERW - (2 * G + nb * G + 4) * 4) / (Wd * 4);
             float accr[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) accr[k] = 0.0f;
-            const int per_chunk = (NW * Ge::PERW - hdr * 4) / (Wd * 4);
-            float* stage = M + hdr;
-            const unsigned stage_u = lvk2::smem_u32(stage);
-            auto chunk_issue = [&](int s0) {
-                const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
-                const float* cs = src + (size_t)s0 * Wd;
-                for (int i = tid; i < cnt * Wd / 2; i += NTHR) {
-                    const unsigned d = stage_u + i * 8;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(cs + 2 * i) : "memory");
-                }
-                cpa_commit();
-            };
-            chunk_issue(0);  // the first chunk of o rows travels with the headers
-            // headers: one round trip
-            for (int i = tid; i < nb * G; i += NTHR) {
-                const float* h = src + (size_t)(i / G) * Wd + (i % G) * (DP + 2);
-                wgt[i] = __ldcg(h);
-                lsv[i] = __ldcg(h + 1);
-            }
-            __syncthreads();
-            LV9_TRACE(11)
-            for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
-                float mm = -INFINITY;
-                for (int s2 = lane; s2 < nb; s2 += 32) mm = fmaxf(mm, wgt[s2 * G + g]);
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
-                float l = 0.0f;
-                for (int s2 = lane; s2 < nb; s2 += 32) {
-                    const float ms = wgt[s2 * G + g];
-                    const float w = ms == -INFINITY ? 0.0f : __expf(ms - mm);
-                    wgt[s2 * G + g] = w;
-                    l += w * lsv[s2 * G + g];
-                }
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
-                if (lane == 0) {
-                    M[g] = mm;
-                    L[g] = l;
-                }
-            }
-            __syncthreads();
-            // o rows through the rings, a chunk of partials per round trip
             for (int s0 = 0; s0 < nb; s0 += per_chunk) {
                 const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
-                if (s0 > 0) chunk_issue(s0);
-                cpa_wait<0>();
+                const float2* cs = reinterpret_cast<const float2*>(src + (size_t)s0 * Wd);
+                for (int i = tid; i < cnt * Wd / 2; i += NTHR) reinterpret_cast<float2*>(stg)[i] = __ldcg(cs + i);
                 __syncthreads();
-                LV9_TRACE(13)
+                if (s0 == 0) {
+                    LV9_TRACE(11)
+                    const bool one = cnt == nb;  // headers from the staged copy when it holds them all
+                    auto hdr = [&](int s2, int g, int k) {
+                        return one ? stg[s2 * Wd + g * (DP + 2) + k] : __ldcg(src + (size_t)s2 * Wd + g * (DP + 2) + k);
+                    };
+                    for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
+                        float mm = -INFINITY;
+                        for (int s2 = lane; s2 < nb; s2 += 32) mm = fmaxf(mm, hdr(s2, g, 0));
+#pragma unroll
+                        for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
+                        float l = 0.0f;
+                        for (int s2 = lane; s2 < nb; s2 += 32) {
+                            const float ms = hdr(s2, g, 0);
+                            const float w = ms == -INFINITY ? 0.0f : __expf(ms - mm);
+                            wgt[s2 * G + g] = w;
+                            l += w * hdr(s2, g, 1);
+                        }
+#pragma unroll
+                        for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+                        if (lane == 0) {
+                            M[g] = mm;
+                            L[g] = l;
+                        }
+                    }
+                    __syncthreads();
+                }
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int i = tid + k * NTHR;
                     if (i < G * DP) {
                         const int g = i / DP, c = i % DP;
                         float a = accr[k];
-#pragma unroll 8
-                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stage[s2 * Wd + g * (DP + 2) + 2 + c], a);
+#pragma unroll 6
+                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stg[s2 * Wd + g * (DP + 2) + 2 + c], a);
                         accr[k] = a;
                     }
                 }

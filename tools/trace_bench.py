@@ -1,0 +1,76 @@
+"""Per-layer timeline of the bench's CUDA graph (C2, 8 layers back to back): every layer
+kernel writes per-CTA phase stamps; prints, per layer, when its CTAs start (before the
+PDL wait), pass griddepcontrol.wait, finish setup / probe / tasks / partial, and when
+the merge ends, relative to the first layer's first CTA."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2605_06763_b200 import BuildConfig, LouverLayer  # noqa: E402
+
+
+def main():
+    cfg = dict(bench.CONFIGS[os.environ.get("CONFIG", "c2")])
+    L = int(os.environ.get("LAYERS", "8"))
+    G = cfg["G"]
+    layers, qs, taus, outs, bufs = [], [], [], [], []
+    for l in range(L):
+        K, V, Q = bench.gen_layer(cfg, l, 0, os.cpu_count())
+        layer = LouverLayer(cfg["d"], cfg["H_kv"], G, cfg["batch"], cfg["n"],
+                            BuildConfig(S=1, r=bench.CELL, grouping="contiguous", enclosing="aabb"))
+        layer.build(K, V)
+        layers.append(layer)
+        qs.append(torch.from_numpy(Q).cuda())
+        taus.append(torch.from_numpy(bench.taus_device(torch, K, Q, G, bench.SELECTIVITY)).cuda())
+        outs.append(torch.zeros((cfg["batch"], cfg["H_kv"] * G, cfg["d"]), device="cuda"))
+        slots = cfg["batch"] * cfg["H_kv"]
+        buf = torch.zeros((slots * 148, 32), dtype=torch.int64, device="cuda")
+        layer._ctx.lib.lv_debug_trace(layer._ctx.h, buf.data_ptr())
+        bufs.append(buf)
+
+    def step():
+        for l in range(L):
+            layers[l].query_device(qs[l], taus[l], outs[l])
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(200):
+        g.replay()
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.zero_()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    trs = [b.cpu().numpy().astype(np.float64) for b in bufs]
+    trs = [t[t[:, 0] > 0] for t in trs]
+    t0 = min(t[:, 0].min() for t in trs)
+    cols = [(0, "start"), (13, "waited"), (1, "setup"), (2, "probe"), (5, "tasks w0"), (6, "partial"),
+            (8, "won"), (7, "end")]
+    print("layer  " + " ".join(f"{nm:>16s}" for _, nm in cols) + "   (min/max over CTAs, us)")
+    for l, t in enumerate(trs):
+        row = []
+        for i, _ in cols:
+            v = t[:, i][t[:, i] > 0]
+            row.append(f"{(v.min() - t0) / 1e3:7.2f}/{(v.max() - t0) / 1e3:7.2f}" if v.size else " " * 15)
+        print(f"{l:5d}  " + " ".join(f"{x:>16s}" for x in row))
+    ends = [t[:, 7][t[:, 7] > 0].max() for t in trs]
+    print(f"per-layer period (end to end): {np.diff(ends).mean() / 1e3:.2f} us")
+
+
+if __name__ == "__main__":
+    main()

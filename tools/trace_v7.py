@@ -30,7 +30,7 @@ def main():
     out = torch.zeros((cfg["batch"], cfg["H_kv"] * G, cfg["d"]), device="cuda")
     slots = cfg["batch"] * cfg["H_kv"]
     nb = -(-2 * 148 // slots)
-    buf = torch.zeros((slots * nb, 16), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((slots * nb, 32), dtype=torch.int64, device="cuda")
     for _ in range(int(os.environ.get("WARM", "300"))):  # keep the clocks up
         layer.query_device(q, t, out)
     torch.cuda.synchronize()

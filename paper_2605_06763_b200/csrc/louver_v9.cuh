@@ -227,11 +227,13 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         // only writes the open cell). Its stream then overlaps the preceding kernel's tail.
         bool pre = false;
         if (!waited) {
-            const long long c0 = blk + (long long)16 * warp * nb;
-            pre = c0 >= cap_cells || c0 + 15LL * nb < vp.sealed;
+            // sub-blocks 0, 1 (tile warp) and 2 (tile warp + NW) fill the 3-stage ring
+            const long long c0 = blk + (long long)16 * warp * nb, c1 = c0 + (long long)16 * NW * nb;
+            pre = (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) && (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed);
             if (pre) {
                 p_issue(0, cap_cells);
                 p_issue(1, cap_cells);
+                p_issue(2, cap_cells);
             }
             asm volatile("griddepcontrol.wait;\n" ::: "memory");
             waited = true;
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         if (!pre) {
             p_issue(0, cap_cells);
             p_issue(1, cap_cells);
+            p_issue(2, cap_cells);
         }
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
@@ -348,8 +351,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             for (int u = 0;; ++u) {
                 const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
                 if (c0 >= ncells) break;
-                p_issue(u + 2, ncells);
-                cpa_wait<2>();
+                cpa_wait<2>();  // sub-block u landed (u + 1, u + 2 may pend)
                 __syncwarp();
                 const int half = u & 1;
                 if (half == 0) {
@@ -415,6 +417,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     }
                 }
                 __syncwarp();
+                p_issue(u + 3, ncells);  // into the stage just consumed
             }
             cpa_wait<0>();
             __syncwarp();

@@ -14,11 +14,6 @@
 #include "louver_aux.cuh"
 #include "louver_b200.h"
 #include "louver_dispatch.h"
-#include "louver_v10.cuh"
-#include "louver_v11.cuh"
-#include "louver_v12.cuh"
-
-#include <cudaTypedefs.h>
 #include "louver_v2.cuh"
 #include "louver_v9.cuh"
 
@@ -63,8 +58,6 @@ struct Workspace {
     float* part_out = nullptr; // [rows][DP+2]
     int* counts = nullptr;     // [rows][4]
     unsigned short* glist = nullptr;  // [slots][cap_cells + nb] survivor lists (fused kernel, large contexts)
-    unsigned* qent = nullptr;  // [slots][cap / 16] v10 work-queue entries (block + 1; kept zero between launches)
-    int* qctl = nullptr;       // [slots][4] v10 queue counters (kept zero between launches)
 };
 
 }  // namespace
@@ -90,8 +83,6 @@ struct lv_ctx {
     // host mirrors of the device counters
     long long n = 0, indexed = 0, flushes = 0;
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
-    CUtensorMap kmap{};          // bf16: TMA map of the K arena (v10)
-    CUtensorMap smap{};          // bf16: TMA map of the cell summaries (v10)
     std::mutex writer;
 };
 
@@ -122,11 +113,7 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
     unsigned char* stk = take(sizeof(int) * c->slots);
     unsigned char* cmk = take(sizeof(unsigned) * c->slots * (size_t)c->units);
     unsigned char* gl = take(sizeof(unsigned short) * c->slots * ((size_t)c->cap_cells + c->nb));
-    unsigned char* qe = take(sizeof(unsigned) * c->slots * (size_t)(c->cap / 16));
-    unsigned char* qc = take(sizeof(int) * 4 * c->slots);
     if (w) {
-        w->qent = reinterpret_cast<unsigned*>(qe);
-        w->qctl = reinterpret_cast<int*>(qc);
         w->glist = reinterpret_cast<unsigned short*>(gl);
         w->gpart = reinterpret_cast<float*>(gp);
         w->gtickets = reinterpret_cast<int*>(gt);
@@ -141,34 +128,6 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
         w->counts = reinterpret_cast<int*>(cnt);
     }
     return off;
-}
-
-// TMA maps (bf16 only): K arena [slots * cap][DP] and summaries [slots * cap_cells][2 DP],
-// boxes of 64 elements x 16 rows with the 128-byte swizzle the v10 kernel reads.
-int make_maps(lv_ctx* c) {
-    if (c->cfg.dtype != LV_BF16) return LV_OK;
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q{};
-        void* fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn)
-            return fail(LV_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    auto one = [&](CUtensorMap* m, void* base, unsigned long long cols, unsigned long long rows) {
-        const cuuint64_t dims[2] = {cols, rows};
-        const cuuint64_t strides[1] = {cols * 2};
-        const cuuint32_t box[2] = {64, 16};
-        const cuuint32_t estr[2] = {1, 1};
-        return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    };
-    if (one(&c->kmap, c->K, (unsigned long long)c->DP, (unsigned long long)c->slots * c->cap) != CUDA_SUCCESS ||
-        one(&c->smap, c->lo, 2ULL * c->DP, (unsigned long long)c->slots * c->cap_cells) != CUDA_SUCCESS)
-        return fail(LV_ERUNTIME, "cuTensorMapEncodeTiled failed");
-    return LV_OK;
 }
 
 int validate(const lv_config* c) {
@@ -354,26 +313,7 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         // cells complete before the last insert enqueued ahead of this query: the insert kernel
         // that may still be draining under PDL writes only the cell of key n - 1
         v5.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
-        static const int k2 = [] { const char* e = getenv("LV_K2"); return e ? atoi(e) : 9; }();
-        if (k2 == 12) {
-            e = lvk12::launch_layer_v12(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
-        } else if (k2 != 10 && k2 != 11) {
-            e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
-        } else {
-            lvk10::V10Params vp{};
-            vp.kmap = c->kmap;
-            vp.smap = c->smap;
-            vp.p = v5.p;
-            vp.qent = w.qent;
-            vp.qctl = w.qctl;
-            vp.qcap = (int)(c->cap / 16);
-            vp.nb = c->nb;
-            vp.slots = c->slots;
-            static const int dbg = [] { const char* e = getenv("LV_DBG"); return e ? atoi(e) : 0; }();
-            vp.dbg = dbg;
-            e = k2 == 11 ? lvk11::launch_layer_v11(c->DP, c->G, vp, c->sms, st, c->layer_geo)
-                         : lvk10::launch_layer_v10(c->DP, c->G, vp, c->sms, st, c->layer_geo);
-        }
+        e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
     } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
         lvk2::V2Params vp{};
         vp.p = p;
@@ -509,10 +449,6 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
     cudaMemset(c->ins_ticket, 0, sizeof(int));
     cudaMemset(c->ws_mem, 0, c->ws_bytes);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup("init", e);
-    if (int rc = make_maps(c)) {
-        lv_destroy(c);
-        return rc;
-    }
     *out = c;
     return LV_OK;
 }
@@ -634,7 +570,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->nb_groups = probe_geo.nb_groups;
     c->nbp = probe_geo.nbp;
     c->cfg.capacity = capacity;
-    return make_maps(c);
+    return LV_OK;
 }
 
 int lv_build(lv_ctx* c, const void* K, const void* V, int64_t n, int src_dtype, int where,

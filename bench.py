@@ -442,25 +442,50 @@ def main():
     except Exception as ex:  # pragma: no cover - library path unavailable
         log(f"sdpa baseline unavailable: {ex}")
 
-    # ---- end to end through the public API with host buffers (pinned)
-    q_host = [torch.empty((B, H_q, d), dtype=torch.float32).pin_memory() for _ in range(L)]
-    t_host = [torch.empty((B, H_q), dtype=torch.float32).pin_memory() for _ in range(L)]
-    for l in range(L):
-        q_host[l].copy_(qs[l].cpu())
-        t_host[l].copy_(taus[l].cpu())
+    # ---- end to end through the public API with host buffers (pinned), one decode step at a
+    # time: the step's q and tau go host->device in one copy each, the L layer queries run
+    # back to back on the stream (lv_query), the L outputs come back in one copy, then the
+    # host waits for the stream. Also reported: one synchronous lv_query(LV_HOST) per layer.
+    q_all_h = torch.stack([q.cpu() for q in qs]).pin_memory()      # [L][B][H_q][d]
+    t_all_h = torch.stack([t.cpu() for t in taus]).pin_memory()    # [L][B][H_q]
+    o_all_h = torch.empty((L, B, H_q, d), dtype=torch.float32).pin_memory()
+    q_all_d, t_all_d = torch.empty_like(q_all_h, device="cuda"), torch.empty_like(t_all_h, device="cuda")
+    o_all_d = torch.empty((L, B, H_q, d), dtype=torch.float32, device="cuda")
+
+    def e2e_step():
+        if world > 1:  # the sharded step: per-layer inputs, shard queries + all-gather + LSE merge
+            for l in range(L):
+                qs[l].copy_(q_all_h[l], non_blocking=True)
+                taus[l].copy_(t_all_h[l], non_blocking=True)
+            step()
+            for l in range(L):
+                o_all_h[l].copy_(outs[l], non_blocking=True)
+        else:
+            q_all_d.copy_(q_all_h, non_blocking=True)
+            t_all_d.copy_(t_all_h, non_blocking=True)
+            for l in range(L):
+                layers[l].query_device(q_all_d[l], t_all_d[l], o_all_d[l])
+            o_all_h.copy_(o_all_d, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
     e2e_steps = max(5, min(50, args.steps))
-    for _ in range(2):
-        for l in range(L):
-            layers[l].query_host(q_host[l].numpy(), t_host[l].numpy())
-    torch.cuda.synchronize()
+    for _ in range(3):
+        e2e_step()
     t1 = time.perf_counter()
     for _ in range(e2e_steps):
-        for l in range(L):
-            if world > 1:
-                o = layers[l].query_host(q_host[l].numpy(), t_host[l].numpy())
-            else:
-                o = layers[l].query_host(q_host[l].numpy(), t_host[l].numpy())
+        e2e_step()
     e2e_us = (time.perf_counter() - t1) * 1e6 / (e2e_steps * L)
+    # one synchronous host-buffer call per layer (lv_query with LV_HOST)
+    qn = [q_all_h[l].numpy() for l in range(L)]
+    tn = [t_all_h[l].numpy() for l in range(L)]
+    on = [o_all_h[l].numpy() for l in range(L)]
+    for l in range(L):
+        layers[l].query_host(qn[l], tn[l], out=on[l])
+    t2 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for l in range(L):
+            layers[l].query_host(qn[l], tn[l], out=on[l])
+    e2e_sync_us = (time.perf_counter() - t2) * 1e6 / (e2e_steps * L)
     if world > 1:
         t = torch.tensor([e2e_us], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -541,7 +566,10 @@ def main():
                   "speedup_vs_torch_sdpa": (sdpa_us / kern_us) if sdpa_us else None},
         "e2e": {"value": e2e_us, "unit": UNIT, "h2d_bytes_per_step": L * rows * (d + 1) * 4,
                 "d2h_bytes_per_step": L * rows * d * 4,
-                "how": "LouverLayer.query_host (lv_query, LV_HOST): pinned q/tau H2D, kernel, out D2H, sync; per layer"},
+                "how": ("host wall clock per decode step / L: pinned q, tau -> device (one copy each), L x "
+                        "lv_query on the stream, L outputs -> pinned host (one copy), stream sync"),
+                "per_layer_sync_us": e2e_sync_us,
+                "per_layer_sync_how": "one synchronous lv_query(LV_HOST) per layer: pinned q/tau H2D, kernel, pinned out D2H, sync"},
         "clocks": clocks.summary(),
     }
     if cpu is not None:

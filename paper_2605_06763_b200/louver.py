@@ -432,11 +432,15 @@ class LouverLayer:
         check(self._ctx.lib.lv_query(self._ctx.h, C.byref(args)), "lv_query")
 
     def query_host(self, q: np.ndarray, tau: np.ndarray, *, scale: float = 0.0,
-                   strict: bool = False, want_counts: bool = False):
-        """Host buffers in and out (copies inside the call): returns out[, counts]."""
+                   strict: bool = False, want_counts: bool = False, out: np.ndarray | None = None):
+        """Host buffers in and out (copies inside the call): returns out[, counts].
+        ``out`` may be a caller-owned (ideally pinned) float32 [batch][H_q][d] buffer."""
         q = np.ascontiguousarray(q, dtype=np.float32)
         tau = np.ascontiguousarray(tau, dtype=np.float32)
-        out = np.zeros((self.batch, self.H_q, self.d), dtype=np.float32)
+        if out is None:
+            out = np.zeros((self.batch, self.H_q, self.d), dtype=np.float32)
+        elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size != self.batch * self.H_q * self.d:
+            raise ValueError("query_host: out must be a C-contiguous float32 [batch][H_q][d] array")
         counts = np.zeros((self.batch, self.H_q, 4), dtype=np.int32) if want_counts else None
         args = _capi.lv_query_args(
             q=_ptr(q), tau=_ptr(tau), scale=float(scale), algo=1, strict=1 if strict else 0,

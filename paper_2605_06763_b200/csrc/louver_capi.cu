@@ -544,6 +544,9 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     probe_geo.slots = c->slots;
     probe_geo.rows = c->rows;
     probe_geo.cap = ncap;
+    probe_geo.r = c->r;
+    probe_geo.r_log2 = c->r_log2;
+    probe_geo.cap_cells = ncells;  // sizes the survivor-list scratch
     choose_splits(&probe_geo);
     const size_t wsb = carve(&probe_geo, nullptr, nullptr);
     if ((e = cudaMalloc(&ws, wsb)) != cudaSuccess) return undo(e);

@@ -310,6 +310,8 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         v5.gmax = nullptr;
         v5.p.tot_trace = c->trace;
         v5.glist = w.glist;
+        static const int dbg = [] { const char* e = getenv("LV_DBG"); return e ? atoi(e) : 0; }();
+        v5.dbg = dbg;
         // cells complete before the last insert enqueued ahead of this query: the insert kernel
         // that may still be draining under PDL writes only the cell of key n - 1
         v5.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;

@@ -55,6 +55,8 @@ struct V5Params {
     unsigned short* glist;     // v9: survivor lists in global scratch when they outgrow smem (else null)
     int list_cap;              // v9: entries per CTA list
     long long sealed;          // v9: cells complete when the query was enqueued (immutable summaries)
+    int dbg;                   // v9: timing experiments only (LV_DBG; output invalid): 1 no merge,
+                               //     2 no CTA partial and no merge, 4 ticket without the merge body
 };
 
 // physical element of logical (k-step t, fragment element e in 0..3) for lane q:

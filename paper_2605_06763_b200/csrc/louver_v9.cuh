@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         if (!waited) {
             // sub-blocks 0, 1 (tile warp) and 2 (tile warp + NW) fill the 3-stage ring
             const long long c0 = blk + (long long)16 * warp * nb, c1 = c0 + (long long)16 * NW * nb;
-            pre = (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) && (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed);
+            pre = (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) && (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed) &&
+                  !(vp.dbg & 8);  // timing experiment: no prefetch before the wait
             if (pre) {
                 p_issue(0, cap_cells);
                 p_issue(1, cap_cells);
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         // ---- warp partials -> CTA partial [G][DP+2] (m, l, o)
         constexpr int Wd = G * (DP + 2);
+        if (vp.dbg & 2) continue;  // timing experiment: no partial, no merge (output invalid)
         float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Wd] over the rings
         float* shw = red;                                           // [NW][G] weights
         __syncthreads();
@@ -743,6 +745,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(6)
 
         // ---- phase C: the last CTA of the team merges the nb partials
+        if (vp.dbg & 1) continue;  // timing experiment: no merge (output invalid)
         int* ticket = vp.stickets + slot;
         __syncthreads();
         if (tid == 0) iscr[1] = atom_add_acq_rel(ticket, 1) == nb - 1;

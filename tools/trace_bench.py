@@ -69,6 +69,12 @@ def main():
             row.append(f"{(v.min() - t0) / 1e3:7.2f}/{(v.max() - t0) / 1e3:7.2f}" if v.size else " " * 15)
         print(f"{l:5d}  " + " ".join(f"{x:>16s}" for x in row))
     ends = [t[:, 7][t[:, 7] > 0].max() for t in trs]
+    for l, t in enumerate(trs):
+        w = t[t[:, 18] > 0]
+        if w.size:
+            d = lambda a, b: np.median(w[:, b] - w[:, a])
+            print(f"layer {l} merge body cycles: stage {d(18, 19):.0f}  heads {d(19, 20):.0f}  accumulate {d(20, 21):.0f}  "
+                  f"write {d(21, 22):.0f}")
     print(f"per-layer period (end to end): {np.diff(ends).mean() / 1e3:.2f} us")
 
 

@@ -467,10 +467,15 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const long long kb = key0(t);
                     const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks + (size_t)kb * DP) + lane * 16;
                     const unsigned dst = ring + stage * Ge::STAGE;
-                    const long long lim = n - kb - lane / CPR;
+                    if (kb + 16 <= n) {  // the common case: the whole block is stored keys
 #pragma unroll
-                    for (int k = 0; k < CPR / 2; ++k)
-                        cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, (long long)(k * RPI) < lim);
+                        for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512);
+                    } else {
+                        const long long lim = n - kb - lane / CPR;
+#pragma unroll
+                        for (int k = 0; k < CPR / 2; ++k)
+                            cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, (long long)(k * RPI) < lim);
+                    }
                 }
                 cpa_commit();
             };
@@ -571,11 +576,11 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     mloc = fmaxf(mloc, s[j]);
                     amask |= row_bits<G>(__ballot_sync(0xffffffffu, att)) << (j * (32 / G));
                 }
-                if (lane == 0) t_keys += (k0 + 16 <= n) ? 16 : (n > k0 ? n - k0 : 0);
+                if (p.totals && lane == 0) t_keys += (k0 + 16 <= n) ? 16 : (n > k0 ? n - k0 : 0);
                 float alpha = 1.0f;
                 unsigned nbf[4] = {0u, 0u, 0u, 0u};
                 if (amask) {
-                    if (lane == 0) t_vals += __popc(amask);
+                    if (p.totals && lane == 0) t_vals += __popc(amask);
 #pragma unroll
                     for (int of = 16; of >= G; of >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, of));
                     // lazy rescale: the reference max moves only when a score exceeds it by

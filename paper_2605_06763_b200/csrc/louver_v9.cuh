@@ -181,10 +181,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #define LV9_TRACE(i) \
     if (trace && tid == 0) trace[i] = lvk2::gtimer();
 
-    // zero the ring once: rows of a V stage that are not loaded meet P = 0
-    for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
-        *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
-    __syncwarp();
+    // (no ring zeroing: a V stage is always the stage of its task's K block, loaded whole,
+    // with rows past n zero-filled, so rows that are not attended hold finite values)
 
     for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
         trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 32 : nullptr;
@@ -206,17 +204,34 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             iscr[3] = 0;  // tasks claimed
         }
         const long long cap_cells = p.cap_cells;
+        // chunk k*32 + lane of a 16-row sub-block: row k*RPI0 + lane/CPR, chunk lane%CPR; the
+        // swizzled destination repeats with period P0 in k (precomputed per lane)
+        constexpr int RPI0 = 32 / CPR, P0 = 8 / RPI0;
+        unsigned pdoff[P0];
+#pragma unroll
+        for (int kk = 0; kk < P0; ++kk) {
+            const int row = kk * RPI0 + lane / CPR, c = lane % CPR;
+            pdoff[kk] = row * RB + ((c ^ (row & 7)) << 4);
+        }
+        const size_t plane = ((size_t)(lane / CPR) * nb * (4 * DP)) + (size_t)(lane % CPR) * 16;
+        const size_t pkstride = (size_t)RPI0 * nb * (4 * DP);
         auto p_issue = [&](int u, long long bound) {
             const long long c0 = blk + (long long)16 * (warp + (u >> 1) * NW) * nb;
             if (c0 < bound) {
                 const unsigned dst = ring + (u % 3) * Ge::STAGE;
                 const size_t hoff = (size_t)(u & 1) * DP * 2;
+                if (c0 + 15LL * nb < cap_cells) {  // every row inside the arena
+                    const unsigned char* src = sumb + (size_t)c0 * (4 * DP) + hoff + plane;
 #pragma unroll
-                for (int k = 0; k < CPR / 2; ++k) {
-                    const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
-                    long long cell = c0 + (long long)row * nb;
-                    cell = cell < cap_cells ? cell : cap_cells - 1;  // past the arena: any row, ignored
-                    cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), sumb + (size_t)cell * (4 * DP) + hoff + c * 16);
+                    for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P0) * 8 * RB + pdoff[k % P0], src + k * pkstride);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < CPR / 2; ++k) {
+                        const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
+                        long long cell = c0 + (long long)row * nb;
+                        cell = cell < cap_cells ? cell : cap_cells - 1;  // past the arena: any row, ignored
+                        cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), sumb + (size_t)cell * (4 * DP) + hoff + c * 16);
+                    }
                 }
             }
             cpa_commit();
@@ -835,10 +850,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             LV9_TRACE(7)
         }
         __syncthreads();
-        // the ring was used as merge scratch: restore zeros for the next slot
-        for (int i = lane; i < 3 * Ge::STAGE / 16; i += 32)
-            *reinterpret_cast<uint4*>(wbase + i * 16) = make_uint4(0u, 0u, 0u, 0u);
-        __syncthreads();
+        __syncthreads();  // the rings served as merge scratch
     }
 #undef LV9_TRACE
 }

@@ -142,6 +142,7 @@ struct C9 {
 template <int DP, int G>
 __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ V5Params vp) {
     using Ge = C9<DP, G>;
+    constexpr bool PACK = G <= 4;  // P.V: hi and lo parts of P share one n-tile
     constexpr int NW = Ge::NW, NTHR = Ge::NTHR, NT = Ge::NT, NTP = Ge::NTP, KS = Ge::KS, CPR = Ge::CPR,
                   RB = Ge::RB, PPL = Ge::PPL, MT = Ge::MT, CT = Ge::CT;
     const QueryParams& p = vp.p;
@@ -616,19 +617,28 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     // B fragment of P: k = rows (2q, 2q+1 | 2q+8, 2q+9), n = head lane/4
                     const int hn = lane >> 2;
                     float pv4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                    if (hn < G) {
-                        pv4[0] = pbuf[(2 * q4) * G + hn];
-                        pv4[1] = pbuf[(2 * q4 + 1) * G + hn];
-                        pv4[2] = pbuf[(2 * q4 + 8) * G + hn];
-                        pv4[3] = pbuf[(2 * q4 + 9) * G + hn];
+                    // G <= 4: one n-tile carries both parts, column h = hi part of head h,
+                    // column G + h = lo part (summed after the loop); G = 8: two n-tiles
+                    const int hh = PACK ? hn % G : hn;
+                    if (PACK ? hn < 2 * G : hn < G) {
+                        pv4[0] = pbuf[(2 * q4) * G + hh];
+                        pv4[1] = pbuf[(2 * q4 + 1) * G + hh];
+                        pv4[2] = pbuf[(2 * q4 + 8) * G + hh];
+                        pv4[3] = pbuf[(2 * q4 + 9) * G + hh];
                     }
                     float lo4[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) lo4[e] = pv4[e] - lvk2::bf_val(lvk2::bf_bits(pv4[e]));
-                    nbf[0] = bf2(pv4[0], pv4[1]);
-                    nbf[1] = bf2(pv4[2], pv4[3]);
-                    nbf[2] = bf2(lo4[0], lo4[1]);
-                    nbf[3] = bf2(lo4[2], lo4[3]);
+                    if (PACK) {
+                        const bool lo = hn >= G;
+                        nbf[0] = lo ? bf2(lo4[0], lo4[1]) : bf2(pv4[0], pv4[1]);
+                        nbf[1] = lo ? bf2(lo4[2], lo4[3]) : bf2(pv4[2], pv4[3]);
+                    } else {
+                        nbf[0] = bf2(pv4[0], pv4[1]);
+                        nbf[1] = bf2(pv4[2], pv4[3]);
+                        nbf[2] = bf2(lo4[0], lo4[1]);
+                        nbf[3] = bf2(lo4[2], lo4[3]);
+                    }
                 }
                 __syncwarp();  // K(t) and pbuf reads done
                 // -- V(t): attended rows into K(t)'s stage (same row positions)
@@ -660,7 +670,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         unsigned a[4];
                         ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
                         mma16816(o[mt], a, pb[0], pb[1]);
-                        mma16816(o[mt], a, pb[2], pb[3]);
+                        if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                     }
                 }
                 if (__any_sync(0xffffffffu, alpha != 1.0f)) {
@@ -690,10 +700,22 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     unsigned a[4];
                     ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
                     mma16816(o[mt], a, pb[0], pb[1]);
-                    mma16816(o[mt], a, pb[2], pb[3]);
+                    if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                 }
             }
             __syncwarp();
+        }
+        if (PACK) {  // fold the lo-part columns (G + h) into the hi-part columns (h)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                if (G == 1) {
+                    o[mt][0] += o[mt][1];
+                    o[mt][2] += o[mt][3];
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[mt][e] += __shfl_xor_sync(0xffffffffu, o[mt][e], G / 2);
+                }
+            }
         }
         LV9_TRACE(5)
 

@@ -198,6 +198,41 @@ int lv_dense_decode(lv_ctx* ctx, const float* q, float scale, int where, float* 
  * into out[rows][d] (device pointers). Empty shards carry m = -inf, l = 0. */
 int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream);
 
+/* --- Threshold oracle (threshold.hpp:9-53, threshold.cpp:40-103) --------------
+ * OracleVariant (threshold.hpp:9), same order. */
+#define LV_TAU_MAX 0      /* "max":      the largest sample score */
+#define LV_TAU_TOPK 1     /* "topk:m":   the m-th largest */
+#define LV_TAU_GAP 2      /* "gap":      cut at the largest gap between sorted scores */
+#define LV_TAU_MEANMAX 3  /* "meanmax":  (max + mean) / 2, mean in double */
+#define LV_TAU_BUDGET 4   /* "budget:a": nearest-rank (1 - a) quantile */
+
+/* Reservoir (threshold.hpp:29-50): Algorithm R over a key stream, with the
+ * reference's std::mt19937_64 + uniform_int_distribution draws, so a reservoir
+ * with the same capacity and seed holds the same ids after the same updates.
+ * It samples arena row ids (host bookkeeping; keys stay in the HBM arena). */
+typedef struct lv_reservoir lv_reservoir;
+int lv_reservoir_create(int64_t capacity, uint64_t seed, lv_reservoir** out); /* capacity >= 1 */
+int lv_reservoir_destroy(lv_reservoir* res);
+/* Reservoir::update (threshold.cpp:40-55); *slot (optional) = the position
+ * written, or -1 when the id was not admitted. */
+int lv_reservoir_update(lv_reservoir* res, uint32_t id, int64_t* slot);
+int64_t lv_reservoir_size(const lv_reservoir* res);
+int64_t lv_reservoir_seen(const lv_reservoir* res);
+int64_t lv_reservoir_capacity(const lv_reservoir* res);
+/* Copies the size() sampled ids, in reservoir order, to host ids[]. */
+int lv_reservoir_ids(const lv_reservoir* res, uint32_t* ids);
+
+/* estimate_tau (threshold.cpp:63-103) for every q head on the device: the
+ * reservoir of kv slot s is ids[s * ld .. s * ld + count) (arena rows < lv_n),
+ * q is [batch][H_q][d] fp32, tau[batch][H_q] receives the estimates; ids, q
+ * and tau are host or device per `where`. Scores use the normative dot on the
+ * arena rows (bf16 arenas: the stored bf16 keys). Errors as the reference's
+ * std::invalid_argument: LV_EINVAL for an invalid OracleConfig (topk m < 1,
+ * budget alpha outside (0, 1)), an empty reservoir, topk count < m, gap
+ * count < 2; count > 8192 is LV_EINVAL too (one CTA sorts the sample). */
+int lv_estimate_tau(lv_ctx* ctx, const uint32_t* ids, int64_t count, int64_t ld, const float* q,
+                    int variant, int m, double alpha, int where, float* tau, void* stream);
+
 /* Host-side synthetic streams with the reference laws (io.cpp:89-206);
  * exported by liblouver_synth.so. */
 int lv_synth_keys(int64_t n, int d, uint64_t seed, float* out);

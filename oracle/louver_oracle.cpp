@@ -763,6 +763,100 @@ float lvo_kth_score(const float* keys, int64_t n, int d, const float* q, int64_t
     return s[static_cast<std::size_t>(k - 1)];
 }
 
+// threshold.hpp:29-50 — Algorithm R with the reference's engine and distribution
+struct lvo_reservoir {
+    std::size_t capacity;
+    std::vector<uint32_t> ids;
+    std::size_t seen = 0;
+    std::mt19937_64 rng;
+};
+
+lvo_reservoir* lvo_reservoir_create(int64_t capacity, uint64_t seed) {
+    if (capacity < 1) return nullptr;  // threshold.hpp:33
+    auto* r = new lvo_reservoir{static_cast<std::size_t>(capacity), {}, 0, std::mt19937_64(seed)};
+    return r;
+}
+
+void lvo_reservoir_destroy(lvo_reservoir* r) { delete r; }
+
+// threshold.cpp:40-55
+int64_t lvo_reservoir_update(lvo_reservoir* r, uint32_t id) {
+    ++r->seen;
+    if (r->ids.size() < r->capacity) {
+        r->ids.push_back(id);
+        return static_cast<int64_t>(r->ids.size() - 1);
+    }
+    std::uniform_int_distribution<std::size_t> pick(0, r->seen - 1);
+    const std::size_t slot = pick(r->rng);
+    if (slot < r->capacity) {
+        r->ids[slot] = id;
+        return static_cast<int64_t>(slot);
+    }
+    return -1;
+}
+
+int64_t lvo_reservoir_size(const lvo_reservoir* r) { return static_cast<int64_t>(r->ids.size()); }
+int64_t lvo_reservoir_seen(const lvo_reservoir* r) { return static_cast<int64_t>(r->seen); }
+void lvo_reservoir_ids(const lvo_reservoir* r, uint32_t* out) {
+    if (!r->ids.empty()) std::memcpy(out, r->ids.data(), sizeof(uint32_t) * r->ids.size());
+}
+
+// threshold.cpp:63-103 (OracleConfig::validate: threshold.hpp:17-22)
+int lvo_estimate_tau(const float* keys, int64_t n_, int d, const float* q, int variant, int m,
+                     double alpha, float* tau) {
+    return guarded([&] {
+        if (variant == 1 && m < 1) throw std::invalid_argument("OracleConfig: m >= 1 required");
+        if (variant == 4 && !(alpha > 0.0 && alpha < 1.0))
+            throw std::invalid_argument("OracleConfig: 0 < alpha < 1 required");
+        if (variant < 0 || variant > 4) throw std::invalid_argument("unknown oracle variant");
+        const std::size_t n = static_cast<std::size_t>(n_);
+        if (n == 0) throw std::invalid_argument("estimate_tau: empty reservoir");
+        std::vector<float> scores(n);
+        lvo_scores(keys, n_, d, q, scores.data());
+        std::sort(scores.begin(), scores.end(), std::greater<>());
+        float r = 0.0f;
+        switch (variant) {
+            case 0:
+                r = scores[0];
+                break;
+            case 1:
+                if (n < static_cast<std::size_t>(m))
+                    throw std::invalid_argument("estimate_tau: sample smaller than topk rank");
+                r = scores[static_cast<std::size_t>(m - 1)];
+                break;
+            case 2: {
+                if (n < 2) throw std::invalid_argument("estimate_tau: gap needs >= 2 samples");
+                std::size_t best = 0;
+                float best_gap = scores[0] - scores[1];
+                for (std::size_t i = 1; i + 1 < n; ++i) {
+                    const float gap = scores[i] - scores[i + 1];
+                    if (gap > best_gap) {
+                        best_gap = gap;
+                        best = i;
+                    }
+                }
+                r = scores[best];
+                break;
+            }
+            case 3: {
+                double mean = 0.0;
+                for (float s : scores) mean += s;
+                mean /= static_cast<double>(n);
+                r = static_cast<float>((double(scores[0]) + mean) / 2.0);
+                break;
+            }
+            case 4: {
+                const auto idx = static_cast<std::size_t>(std::min<double>(
+                    std::ceil((1.0 - alpha) * static_cast<double>(n)), static_cast<double>(n - 1)));
+                r = scores[n - 1 - idx];
+                break;
+            }
+        }
+        *tau = r;
+        return LVO_OK;
+    });
+}
+
 int lvo_sparse_attention(const float* keys, const float* values, int64_t n, int d,
                          const uint32_t* buffer_ids, int64_t nbuf, const uint32_t* sel_ids,
                          int64_t nsel, const float* q, float scale, float* out, float* weights,

@@ -114,8 +114,22 @@ int lvo_assign_groups(const float* points, int64_t m, int w, const lvo_build_con
 int lvo_enclose_group(const float* points, int64_t m, int w, int kind, float* center,
                       float* radius, float* lo, float* hi);
 
-/* --- Reference threshold oracle (threshold.cpp) is out of scope; the bench
- *     passes a fixed τ = exact k-th largest normative score. --------------- */
+/* --- Threshold oracle (threshold.hpp:9-53, threshold.cpp:40-103). The bench
+ *     itself passes a fixed τ = exact k-th largest normative score. ---------- */
+/* Reservoir (threshold.hpp:29-50) over ids; update = threshold.cpp:40-55.
+ * lvo_reservoir_update returns the position written, or -1. */
+typedef struct lvo_reservoir lvo_reservoir;
+lvo_reservoir* lvo_reservoir_create(int64_t capacity, uint64_t seed);
+void lvo_reservoir_destroy(lvo_reservoir* r);
+int64_t lvo_reservoir_update(lvo_reservoir* r, uint32_t id);
+int64_t lvo_reservoir_size(const lvo_reservoir* r);
+int64_t lvo_reservoir_seen(const lvo_reservoir* r);
+void lvo_reservoir_ids(const lvo_reservoir* r, uint32_t* out);
+/* estimate_tau (threshold.cpp:63-103) over the n sampled keys [n][d];
+ * variant as OracleVariant (threshold.hpp:9): 0 max, 1 topk, 2 gap, 3 meanmax,
+ * 4 budget. Returns LVO_EINVAL for the reference's invalid_argument cases. */
+int lvo_estimate_tau(const float* keys, int64_t n, int d, const float* q, int variant, int m,
+                     double alpha, float* tau);
 /* k-th largest normative score (1-based k) over keys [0, n). */
 float lvo_kth_score(const float* keys, int64_t n, int d, const float* q, int64_t k);
 

@@ -41,6 +41,13 @@ _SIGS = {
     "lvo_layout": (C.c_int, [C.c_int, C.c_int, _P]),
     "lvo_scores": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
     "lvo_kth_score": (C.c_float, [_P, C.c_int64, C.c_int, _P, C.c_int64]),
+    "lvo_reservoir_create": (_P, [C.c_int64, C.c_uint64]),
+    "lvo_reservoir_destroy": (None, [_P]),
+    "lvo_reservoir_update": (C.c_int64, [_P, C.c_uint32]),
+    "lvo_reservoir_size": (C.c_int64, [_P]),
+    "lvo_reservoir_seen": (C.c_int64, [_P]),
+    "lvo_reservoir_ids": (None, [_P, _P]),
+    "lvo_estimate_tau": (C.c_int, [_P, C.c_int64, C.c_int, _P, C.c_int, C.c_int, C.c_double, _P]),
     "lvo_sparse_attention": (C.c_int, [_P, _P, C.c_int64, C.c_int, _P, C.c_int64, _P, C.c_int64, _P,
                                        C.c_float, _P, _P, _I64P]),
     "lvo_cache_create": (C.c_int, [C.c_int, C.POINTER(lvo_build_config), C.c_int64, C.POINTER(_P)]),
@@ -152,6 +159,44 @@ def kth_score(keys, q, k: int) -> np.float32:
     keys, q = _f32(keys), _f32(q)
     n, d = keys.shape
     return np.float32(lib().lvo_kth_score(keys.ctypes.data, n, d, q.ctypes.data, k))
+
+
+class Reservoir:
+    """threshold.hpp:29-50 over ids (the oracle's restatement; test-only)."""
+
+    def __init__(self, capacity: int = 256, seed: int = 0):
+        if capacity < 1:
+            raise ValueError("Reservoir: capacity >= 1 required")
+        self._h = lib().lvo_reservoir_create(capacity, seed)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().lvo_reservoir_destroy(self._h)
+            self._h = None
+
+    def update(self, key_id: int) -> int:
+        return int(lib().lvo_reservoir_update(self._h, key_id))
+
+    def size(self) -> int:
+        return int(lib().lvo_reservoir_size(self._h))
+
+    def seen(self) -> int:
+        return int(lib().lvo_reservoir_seen(self._h))
+
+    def ids(self) -> np.ndarray:
+        out = np.empty((self.size(),), np.uint32)
+        lib().lvo_reservoir_ids(self._h, out.ctypes.data)
+        return out
+
+
+def estimate_tau(sample_keys, q, variant: int, m: int = 2, alpha: float = 0.1) -> np.float32:
+    """threshold.cpp:63-103 over the sampled keys [n][d]; variant as OracleVariant."""
+    keys, q = _f32(sample_keys), _f32(q)
+    n, d = keys.shape if keys.ndim == 2 else (0, q.shape[0])
+    out = np.zeros((1,), np.float32)
+    _check(lib().lvo_estimate_tau(keys.ctypes.data if n else None, n, d, q.ctypes.data, variant, m, alpha,
+                                  out.ctypes.data))
+    return out[0]
 
 
 def sparse_attention(keys, values, buffer_ids, selected_ids, q, scale):

@@ -7,6 +7,14 @@ include/louver_b200.h. See DESIGN.md.
 """
 from ._capi import LouverError, LIB_PATH, SYNTH_PATH  # noqa: F401
 from .sharding import ShardedLayer, gather_partials, insert_owner, shard_range  # noqa: F401
+from .threshold import (  # noqa: F401
+    OracleConfig,
+    OracleVariant,
+    Reservoir,
+    estimate_tau,
+    estimate_tau_layer,
+    parse_oracle,
+)
 from .louver import (  # noqa: F401
     AttentionResult,
     BuildConfig,
@@ -25,4 +33,5 @@ __all__ = [
     "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
     "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
+    "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
 ]

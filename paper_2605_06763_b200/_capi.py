@@ -17,6 +17,7 @@ LV_OK, LV_EMPTY, LV_EINVAL, LV_ERANGE, LV_ERUNTIME, LV_ENODEV = 0, 1, -1, -2, -3
 LV_F32, LV_BF16 = 0, 1
 LV_HOST, LV_DEVICE = 0, 1
 LV_ALGO_FULL_SUBSPACE, LV_ALGO_TA = 0, 1
+LV_TAU_MAX, LV_TAU_TOPK, LV_TAU_GAP, LV_TAU_MEANMAX, LV_TAU_BUDGET = 0, 1, 2, 3, 4
 
 
 class lv_config(C.Structure):
@@ -101,6 +102,14 @@ _SIGS = {
     ),
     "lv_dense_decode": (C.c_int, [_P, _P, C.c_float, C.c_int, _P, _P, _P]),
     "lv_lse_merge": (C.c_int, [_P, C.c_int, C.c_int64, C.c_int, _P, _P]),
+    "lv_reservoir_create": (C.c_int, [C.c_int64, C.c_uint64, C.POINTER(_P)]),
+    "lv_reservoir_destroy": (C.c_int, [_P]),
+    "lv_reservoir_update": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_int64)]),
+    "lv_reservoir_size": (C.c_int64, [_P]),
+    "lv_reservoir_seen": (C.c_int64, [_P]),
+    "lv_reservoir_capacity": (C.c_int64, [_P]),
+    "lv_reservoir_ids": (C.c_int, [_P, _P]),
+    "lv_estimate_tau": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P]),
 }
 
 _SYNTH_SIGS = {

@@ -8,11 +8,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
 #include "louver_aux.cuh"
 #include "louver_b200.h"
+#include "louver_threshold.cuh"
 #include "louver_dispatch.h"
 #include "louver_v2.cuh"
 #include "louver_v9.cuh"
@@ -792,6 +794,120 @@ int lv_bitmap_to_ids(const uint32_t* bits, int64_t words, int64_t rows, int64_t 
                                                                   count);
     LV_CUDA(cudaGetLastError());
     return LV_OK;
+}
+
+// ---- threshold oracle (threshold.hpp:29-50, threshold.cpp:40-103) ----------------------
+
+struct lv_reservoir {
+    size_t capacity;
+    std::vector<uint32_t> ids;
+    size_t seen = 0;
+    std::mt19937_64 rng;
+    lv_reservoir(size_t cap, uint64_t seed) : capacity(cap), rng(seed) {}
+};
+
+int lv_reservoir_create(int64_t capacity, uint64_t seed, lv_reservoir** out) {
+    if (!out) return fail(LV_EINVAL, "lv_reservoir_create: null out");
+    if (capacity < 1) return fail(LV_EINVAL, "Reservoir: capacity >= 1 required");  // threshold.hpp:33
+    *out = new lv_reservoir((size_t)capacity, seed);
+    return LV_OK;
+}
+
+int lv_reservoir_destroy(lv_reservoir* res) {
+    delete res;
+    return LV_OK;
+}
+
+int lv_reservoir_update(lv_reservoir* res, uint32_t id, int64_t* slot) {
+    if (!res) return fail(LV_EINVAL, "lv_reservoir_update: null reservoir");
+    ++res->seen;
+    int64_t at = -1;
+    if (res->ids.size() < res->capacity) {
+        at = (int64_t)res->ids.size();
+        res->ids.push_back(id);
+    } else {
+        // item t replaces a uniform position with probability capacity / t: the
+        // same distribution object and engine calls as threshold.cpp:49-54
+        std::uniform_int_distribution<std::size_t> pick(0, res->seen - 1);
+        const std::size_t s = pick(res->rng);
+        if (s < res->capacity) {
+            res->ids[s] = id;
+            at = (int64_t)s;
+        }
+    }
+    if (slot) *slot = at;
+    return LV_OK;
+}
+
+int64_t lv_reservoir_size(const lv_reservoir* res) { return res ? (int64_t)res->ids.size() : -1; }
+int64_t lv_reservoir_seen(const lv_reservoir* res) { return res ? (int64_t)res->seen : -1; }
+int64_t lv_reservoir_capacity(const lv_reservoir* res) { return res ? (int64_t)res->capacity : -1; }
+
+int lv_reservoir_ids(const lv_reservoir* res, uint32_t* ids) {
+    if (!res || !ids) return fail(LV_EINVAL, "lv_reservoir_ids: null argument");
+    if (!res->ids.empty()) std::memcpy(ids, res->ids.data(), sizeof(uint32_t) * res->ids.size());
+    return LV_OK;
+}
+
+int lv_estimate_tau(lv_ctx* c, const uint32_t* ids, int64_t count, int64_t ld, const float* q, int variant,
+                    int m, double alpha, int where, float* tau, void* stream) {
+    if (!c || !ids || !q || !tau) return fail(LV_EINVAL, "lv_estimate_tau: null argument");
+    // OracleConfig::validate (threshold.hpp:17-22), then estimate_tau's own checks
+    if (variant < LV_TAU_MAX || variant > LV_TAU_BUDGET) return fail(LV_EINVAL, "estimate_tau: unknown variant");
+    if (variant == LV_TAU_TOPK && m < 1) return fail(LV_EINVAL, "OracleConfig: m >= 1 required");
+    if (variant == LV_TAU_BUDGET && !(alpha > 0.0 && alpha < 1.0))
+        return fail(LV_EINVAL, "OracleConfig: 0 < alpha < 1 required");
+    if (count <= 0) return fail(LV_EINVAL, "estimate_tau: empty reservoir");
+    if (variant == LV_TAU_TOPK && count < m) return fail(LV_EINVAL, "estimate_tau: sample smaller than topk rank");
+    if (variant == LV_TAU_GAP && count < 2) return fail(LV_EINVAL, "estimate_tau: gap needs >= 2 samples");
+    if (count > 8192) return fail(LV_EINVAL, "estimate_tau: reservoir larger than 8192 on the device");
+    if (ld < count) return fail(LV_EINVAL, "estimate_tau: ld < count");
+    const size_t n = (size_t)count;
+    int mode = lvkt::kPick, pick = 0;
+    if (variant == LV_TAU_TOPK) {
+        pick = m - 1;
+    } else if (variant == LV_TAU_GAP) {
+        mode = lvkt::kGap;
+    } else if (variant == LV_TAU_MEANMAX) {
+        mode = lvkt::kMeanMax;
+    } else if (variant == LV_TAU_BUDGET) {  // threshold.cpp:98-101, same expression
+        const auto idx = static_cast<std::size_t>(
+            std::min<double>(std::ceil((1.0 - alpha) * static_cast<double>(n)), static_cast<double>(n - 1)));
+        pick = (int)(n - 1 - idx);
+    }
+    cudaStream_t st = S(stream);
+    Workspace w;
+    carve(c, reinterpret_cast<unsigned char*>(c->ws_mem), &w);
+    const uint32_t* idd = ids;
+    uint32_t* ids_tmp = nullptr;
+    if (where == LV_HOST) {
+        for (int64_t s = 0; s < c->slots; ++s)
+            for (int64_t i = 0; i < count; ++i)
+                if ((long long)ids[s * ld + i] >= c->n) return fail(LV_ERANGE, "estimate_tau: id >= n");
+        LV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ids_tmp), sizeof(uint32_t) * c->slots * ld, st));
+        LV_CUDA(cudaMemcpyAsync(ids_tmp, ids, sizeof(uint32_t) * c->slots * ld, cudaMemcpyHostToDevice, st));
+        idd = ids_tmp;
+    }
+    if (int rc = stage_rows(c, w.q, q, where, st)) return rc;
+    float* taud = where == LV_HOST ? w.tau : tau;
+    int np2 = 2;
+    while (np2 < count) np2 <<= 1;
+    const size_t smem = sizeof(float) * (c->DP + np2);
+    const int threads = np2 < 256 ? 128 : 256;
+    if (c->cfg.dtype == LV_BF16)
+        lvkt::estimate_tau_kernel<__nv_bfloat16><<<(unsigned)c->rows, threads, smem, st>>>(
+            reinterpret_cast<const __nv_bfloat16*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, w.q,
+            mode, pick, np2, taud);
+    else
+        lvkt::estimate_tau_kernel<float><<<(unsigned)c->rows, threads, smem, st>>>(
+            reinterpret_cast<const float*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, w.q, mode,
+            pick, np2, taud);
+    LV_CUDA(cudaGetLastError());
+    if (where == LV_HOST) {
+        LV_CUDA(cudaMemcpyAsync(tau, w.tau, sizeof(float) * c->rows, cudaMemcpyDeviceToHost, st));
+        LV_CUDA(cudaFreeAsync(ids_tmp, st));
+    }
+    return sync_if_host(where, st);
 }
 
 int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream) {

@@ -419,6 +419,50 @@ def main():
         dense_ms.append(ka.elapsed_time(kb))
     dense_us = statistics.mean(dense_ms) * 1e3
 
+    # ---- the threshold oracle on the device: estimate_tau for every
+    # q head of a layer from a 256-id reservoir per kv slot (budget:0.05), one launch
+    tau_oracle = None
+    try:
+        from paper_2605_06763_b200 import OracleConfig, OracleVariant, Reservoir, estimate_tau_layer
+
+        res_cap = 256
+        rids = np.zeros((layers[0].batch * layers[0].H_kv, res_cap), np.uint32)
+        n0 = layers[0].n
+        for s_ in range(rids.shape[0]):
+            rv = Reservoir(res_cap, 1000 * s_ + 1)
+            for t_ in range(0, n0, max(1, n0 // 4096)):
+                rv.update(t_)
+            rids[s_] = rv.ids()
+        rids_d = torch.from_numpy(rids).cuda()
+        tcfg = OracleConfig(OracleVariant.Budget, alpha=SELECTIVITY)
+        tau_bufs = [torch.empty_like(taus[0]) for _ in range(L)]
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for l in range(L):
+                estimate_tau_layer(layers[l], rids_d, res_cap, qs[l], tcfg, tau_bufs[l])
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        tg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(tg):
+            for l in range(L):
+                estimate_tau_layer(layers[l], rids_d, res_cap, qs[l], tcfg, tau_bufs[l])
+        tg.replay()
+        torch.cuda.synchronize()
+        tm = []
+        for _ in range(20):
+            ka.record()
+            tg.replay()
+            kb.record()
+            kb.synchronize()
+            tm.append(ka.elapsed_time(kb) / L)
+        tau_oracle = {"us_per_layer": statistics.median(tm) * 1e3, "reservoir": res_cap,
+                      "oracle": f"budget:{SELECTIVITY}", "q_heads": int(qs[0].numel() // d),
+                      "how": "estimate_tau for all q heads of a layer, one launch; CUDA graph of L launches, "
+                             "replay time / L, median of 20"}
+    except Exception as ex:  # pragma: no cover
+        log(f"threshold oracle timing unavailable: {ex}")
+
     # ---- library dense decode for reference: torch SDPA (flash / efficient kernel) on layer 0
     sdpa_us = None
     try:
@@ -559,6 +603,7 @@ def main():
         "keys": {"n": n, "scanned_per_q_head": keys_scanned, "selected_per_q_head": keys_selected,
                  "attended_per_q_head": keys_attended, "loaded_union_per_layer": float(np.mean(tot[:, 2])),
                  "f_scan": keys_scanned / n},
+        "threshold_oracle": tau_oracle,
         "dense": {"us_per_layer": dense_us, "bytes": dense_bytes,
                   "achieved_gbs": dense_bytes / (dense_us * 1e-6) / 1e9,
                   "speedup_vs_dense": dense_us / kern_us,

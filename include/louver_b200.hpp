@@ -12,6 +12,8 @@
 //   louver::LouverCache                    cache.hpp:21-63          -> LouverCache (device-resident store + index)
 //   louver::brute_force_range              query.hpp:44-45          -> brute_force_range(const LouverCache&, ...)
 //   louver::sparse_attention               query.hpp:69-72          -> sparse_attention(const LouverCache&, ...)
+//   louver::OracleConfig / Reservoir       threshold.hpp:9-50       -> OracleConfig / Reservoir (ids of arena rows)
+//   louver::estimate_tau                   threshold.hpp:53         -> estimate_tau(const LouverCache&, res, q, cfg)
 //
 // Differences a caller sees: the store lives in HBM inside the cache, so the
 // free functions take the cache instead of a `const KeyStore&`; `index()` is not
@@ -398,6 +400,62 @@ class LouverLayer {
 // Log-sum-exp merge of P sequence-shard partials [P][rows][d+2] -> out [rows][d].
 inline void lse_merge(const float* partials, int P, std::int64_t rows, int d, float* out, cudaStream_t st) {
     detail::check(lv_lse_merge(partials, P, rows, d, out, st), "lv_lse_merge");
+}
+
+// ---- threshold oracle (threshold.hpp:9-53) -------------------------------------------
+
+enum class OracleVariant { SampleMax = LV_TAU_MAX, SampleTopK = LV_TAU_TOPK, SampleGap = LV_TAU_GAP,
+                           SampleMeanMax = LV_TAU_MEANMAX, Budget = LV_TAU_BUDGET };
+
+struct OracleConfig {  // threshold.hpp:11-23
+    OracleVariant variant = OracleVariant::SampleMax;
+    int m = 2;
+    double alpha = 0.1;
+    void validate() const {
+        if (variant == OracleVariant::SampleTopK && m < 1) throw std::invalid_argument("OracleConfig: m >= 1 required");
+        if (variant == OracleVariant::Budget && !(alpha > 0.0 && alpha < 1.0))
+            throw std::invalid_argument("OracleConfig: 0 < alpha < 1 required");
+    }
+};
+
+// threshold.hpp:29-50. Samples ids of a cache's (append-only) arena rows with the
+// reference's std::mt19937_64 draws; the key argument of update() is accepted for
+// signature parity only.
+class Reservoir {
+  public:
+    explicit Reservoir(std::size_t capacity = 256, std::uint64_t seed = 0) {
+        lv_reservoir* r = nullptr;
+        detail::check(lv_reservoir_create((int64_t)capacity, seed, &r), "Reservoir");
+        res_.reset(r);
+    }
+    void update(KeyId id, ConstVecRef = {}) { detail::check(lv_reservoir_update(res_.get(), id, nullptr), "update"); }
+    std::size_t size() const { return (std::size_t)lv_reservoir_size(res_.get()); }
+    std::size_t seen() const { return (std::size_t)lv_reservoir_seen(res_.get()); }
+    std::size_t capacity() const { return (std::size_t)lv_reservoir_capacity(res_.get()); }
+    std::vector<KeyId> ids() const {
+        std::vector<KeyId> out(size());
+        if (!out.empty()) detail::check(lv_reservoir_ids(res_.get(), out.data()), "ids");
+        return out;
+    }
+
+  private:
+    struct Del {
+        void operator()(lv_reservoir* r) const { lv_reservoir_destroy(r); }
+    };
+    std::unique_ptr<lv_reservoir, Del> res_;
+};
+
+// threshold.cpp:63-103 on the device, over the cache's rows the reservoir sampled.
+inline Scalar estimate_tau(const LouverCache& cache, const Reservoir& res, ConstVecRef q, const OracleConfig& cfg) {
+    cfg.validate();
+    if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    const std::vector<KeyId> ids = res.ids();
+    if (ids.empty()) throw std::invalid_argument("estimate_tau: empty reservoir");
+    Scalar tau = 0.0f;
+    detail::check(lv_estimate_tau(cache.handle(), ids.data(), (int64_t)ids.size(), (int64_t)ids.size(), q.data(),
+                                  static_cast<int>(cfg.variant), cfg.m, cfg.alpha, LV_HOST, &tau, nullptr),
+                  "estimate_tau");
+    return tau;
 }
 
 }  // namespace louver_b200

@@ -888,19 +888,31 @@ int lv_estimate_tau(lv_ctx* c, const uint32_t* ids, int64_t count, int64_t ld, c
         LV_CUDA(cudaMemcpyAsync(ids_tmp, ids, sizeof(uint32_t) * c->slots * ld, cudaMemcpyHostToDevice, st));
         idd = ids_tmp;
     }
-    if (int rc = stage_rows(c, w.q, q, where, st)) return rc;
+    const float* qd = q;
+    if (!(where == LV_DEVICE && c->cfg.d == c->DP)) {
+        if (int rc = stage_rows(c, w.q, q, where, st)) return rc;
+        qd = w.q;
+    }
     float* taud = where == LV_HOST ? w.tau : tau;
-    int np2 = 2;
+    int np2 = 32;  // at least one warp: the sort's shuffle stages need whole warps
     while (np2 < count) np2 <<= 1;
-    const size_t smem = sizeof(float) * (c->DP + np2);
-    const int threads = np2 < 256 ? 128 : 256;
+    const size_t esz = c->cfg.dtype == LV_BF16 ? 2 : 4;
+    const int rpc = c->cfg.dtype == LV_BF16 ? lvkt::stage_rows<__nv_bfloat16>(c->DP) : lvkt::stage_rows<float>(c->DP);
+    const size_t smem = (size_t)rpc * (c->DP * esz + 16) + sizeof(float) * (c->DP + 2 * (size_t)np2);
+    const int threads = np2 <= 1024 ? np2 : 256;  // one score per thread up to 1024
+    if (smem > 48 * 1024) {
+        LV_CUDA(cudaFuncSetAttribute(lvkt::estimate_tau_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        LV_CUDA(cudaFuncSetAttribute(lvkt::estimate_tau_kernel<__nv_bfloat16>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     if (c->cfg.dtype == LV_BF16)
         lvkt::estimate_tau_kernel<__nv_bfloat16><<<(unsigned)c->rows, threads, smem, st>>>(
-            reinterpret_cast<const __nv_bfloat16*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, w.q,
+            reinterpret_cast<const __nv_bfloat16*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, qd,
             mode, pick, np2, taud);
     else
         lvkt::estimate_tau_kernel<float><<<(unsigned)c->rows, threads, smem, st>>>(
-            reinterpret_cast<const float*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, w.q, mode,
+            reinterpret_cast<const float*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, qd, mode,
             pick, np2, taud);
     LV_CUDA(cudaGetLastError());
     if (where == LV_HOST) {

@@ -21,47 +21,118 @@ namespace lvkt {
 
 enum : int { kPick = 0, kGap = 1, kMeanMax = 2 };
 
-__device__ __forceinline__ float to_f(float x) { return x; }
-__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+// rows staged per round: 64 KB of keys (plus one 16-byte pad per row: the dot
+// loop reads one row per thread, 16 bytes at a time, without bank conflicts)
+constexpr int kStageBytes = 65536;
+
+template <typename T>
+__host__ __device__ constexpr int stage_rows(int DP) {
+    return kStageBytes / (DP * (int)sizeof(T)) > 0 ? kStageBytes / (DP * (int)sizeof(T)) : 1;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* f, float) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float* f, __nv_bfloat16) {
+    const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
 
 template <typename T>
 __global__ void estimate_tau_kernel(const T* __restrict__ K, long long cap, int DP, int d, int G,
                                     const uint32_t* __restrict__ ids, long long ld, int cnt,
                                     const float* __restrict__ q, int mode, int pick, int np2,
                                     float* __restrict__ tau) {
-    extern __shared__ float sh[];
-    float* qs = sh;         // [d]
-    float* sc = sh + DP;    // [np2]
+    extern __shared__ __align__(16) float sh[];
+    constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte vector
+    const int vpr = DP / EPV, rstride = vpr + 1;  // vectors per row, staged row stride (padded)
+    const int rpc = stage_rows<T>(DP);
+    uint4* stg = reinterpret_cast<uint4*>(sh);  // [rpc][rstride]
+    float* qs = sh + (size_t)rpc * rstride * 4;  // [DP], zero past d
+    float* sc = qs + DP;                         // [np2]
+    uint32_t* sid = reinterpret_cast<uint32_t*>(sc + np2);  // [cnt] sampled row ids
     const int row = blockIdx.x, slot = row / G;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) qs[c] = q[(size_t)row * DP + c];
-    __syncthreads();
+    for (int c = threadIdx.x; c < DP; c += blockDim.x) qs[c] = c < d ? q[(size_t)row * DP + c] : 0.0f;
     const uint32_t* rid = ids + (size_t)slot * ld;
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        float s = -INFINITY;  // padding sorts behind every finite score
-        if (i < cnt) {
-            const T* k = K + ((size_t)slot * cap + rid[i]) * DP;
-            s = 0.0f;
-#pragma unroll 8
-            for (int c = 0; c < d; ++c) s = __fadd_rn(s, __fmul_rn(qs[c], to_f(k[c])));
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) sid[i] = __ldg(rid + i);
+    const uint4* Kv = reinterpret_cast<const uint4*>(K + (size_t)slot * cap * DP);
+    for (int i = cnt + threadIdx.x; i < np2; i += blockDim.x) sc[i] = -INFINITY;  // sorts behind every score
+    const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
+    for (int base = 0; base < cnt; base += rpc) {
+        const int nr = cnt - base < rpc ? cnt - base : rpc;
+        __syncthreads();  // previous round's rows consumed (ids and qs written)
+        // every row of the round in flight at once (asynchronous copies, one wait)
+        for (int i = threadIdx.x; i < nr * vpr; i += blockDim.x) {
+            const int r = i / vpr, c = i - r * vpr;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s + (unsigned)(r * rstride + c) * 16u),
+                         "l"(Kv + (size_t)sid[base + r] * vpr + c)
+                         : "memory");
         }
-        sc[i] = s;
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+            // normative order (core.hpp:17-21): fp32 multiply, then add, coordinate by coordinate
+            float s = 0.0f;
+            const int nv = (d + EPV - 1) / EPV;
+            for (int v = 0; v < nv; ++v) {
+                float kf[8];
+                unpack8(stg[r * rstride + v], kf, T());
+#pragma unroll
+                for (int e = 0; e < EPV; ++e)
+                    if (v * EPV + e < d) s = __fadd_rn(s, __fmul_rn(qs[v * EPV + e], kf[e]));
+            }
+            sc[base + r] = s;
+        }
     }
     __syncthreads();
     // bitonic sort, descending overall
-    for (int k = 2; k <= np2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-                const int p = i ^ j;
-                if (p > i) {
-                    const float a = sc[i], b = sc[p];
-                    const bool desc = (i & k) == 0;
-                    if (desc ? a < b : a > b) {
-                        sc[i] = b;
-                        sc[p] = a;
+    if (np2 == (int)blockDim.x) {
+        // one score per thread: partners closer than a warp swap through shuffles, only
+        // the log2(np2) - 5 widest distances of each merge go through shared memory.
+        // On equal scores each side keeps its own value, so the multiset is preserved.
+        const int i = threadIdx.x;
+        float v = sc[i];
+        for (int k = 2; k <= np2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                float o;
+                if (j >= 32) {
+                    __syncthreads();
+                    sc[i] = v;
+                    __syncthreads();
+                    o = sc[i ^ j];
+                } else {
+                    o = __shfl_xor_sync(0xffffffffu, v, j);
+                }
+                const bool take_max = ((i & j) == 0) == ((i & k) == 0);
+                v = take_max ? (o > v ? o : v) : (o < v ? o : v);
+            }
+        }
+        __syncthreads();
+        sc[i] = v;
+        __syncthreads();
+    } else {
+        for (int k = 2; k <= np2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const float a = sc[i], b = sc[p];
+                        const bool desc = (i & k) == 0;
+                        if (desc ? a < b : a > b) {
+                            sc[i] = b;
+                            sc[p] = a;
+                        }
                     }
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
     if (threadIdx.x != 0) return;

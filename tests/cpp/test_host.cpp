@@ -192,6 +192,47 @@ static void test_layer_bf16() {
     cudaFree(dcnt);
 }
 
+// threshold.hpp through the host layer: the reservoir's draws equal the oracle's,
+// and the device estimate equals the oracle's for every variant (bit-exact).
+static void test_threshold() {
+    const int d = 64, n = 3000;
+    std::vector<float> K((size_t)n * d);
+    for (size_t i = 0; i < K.size(); ++i) K[i] = std::sin(0.37f * (float)i) + 0.01f * (float)(i % 97);
+    KeyStore store(d);
+    for (int j = 0; j < n; ++j) store.append({K.data() + (size_t)j * d, (size_t)d}, {K.data() + (size_t)j * d, (size_t)d});
+    LouverCache cache(store, BuildConfig{1, 16, GroupingStrategy::Contiguous, EnclosureKind::Aabb, 0}, 128);
+    Reservoir res(256, 42);
+    lvo_reservoir* ref = lvo_reservoir_create(256, 42);
+    for (int j = 0; j < n; ++j) {
+        res.update((KeyId)j);
+        lvo_reservoir_update(ref, (uint32_t)j);
+    }
+    std::vector<uint32_t> rid(256);
+    lvo_reservoir_ids(ref, rid.data());
+    EXPECT(res.ids() == rid, "reservoir draws equal the oracle's");
+    std::vector<float> sample;
+    for (uint32_t id : rid) sample.insert(sample.end(), K.begin() + (size_t)id * d, K.begin() + (size_t)(id + 1) * d);
+    std::vector<float> q(d);
+    for (int c = 0; c < d; ++c) q[c] = std::cos(0.11f * (float)c);
+    const OracleConfig cfgs[] = {{OracleVariant::SampleMax, 2, 0.1}, {OracleVariant::SampleTopK, 7, 0.1},
+                                 {OracleVariant::SampleGap, 2, 0.1}, {OracleVariant::SampleMeanMax, 2, 0.1},
+                                 {OracleVariant::Budget, 2, 0.05}};
+    for (const auto& cfg : cfgs) {
+        float want = 0.0f;
+        lvo_estimate_tau(sample.data(), 256, d, q.data(), (int)cfg.variant, cfg.m, cfg.alpha, &want);
+        const float got = estimate_tau(cache, res, {q.data(), (size_t)d}, cfg);
+        EXPECT(got == want, "estimate_tau variant %d: %g vs oracle %g", (int)cfg.variant, got, want);
+    }
+    bool threw = false;
+    try {
+        estimate_tau(cache, res, {q.data(), (size_t)d}, OracleConfig{OracleVariant::Budget, 2, 1.5});
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "OracleConfig::validate -> std::invalid_argument");
+    lvo_reservoir_destroy(ref);
+}
+
 int main(int argc, char** argv) {
     if (argc > 1 && std::strcmp(argv[1], "--compile-only") == 0) {
         std::printf("%s\n", lv_build_info());
@@ -200,6 +241,7 @@ int main(int argc, char** argv) {
     try {
         test_cache_fp32();
         test_layer_bf16();
+        test_threshold();
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         return 2;

@@ -233,6 +233,12 @@ int lv_reservoir_ids(const lv_reservoir* res, uint32_t* ids);
 int lv_estimate_tau(lv_ctx* ctx, const uint32_t* ids, int64_t count, int64_t ld, const float* q,
                     int variant, int m, double alpha, int where, float* tau, void* stream);
 
+/* Decode-loop verification (bench.cpp:83-86): adds to *violations (DEVICE
+ * int32) the number of rows whose two DEVICE bitmaps [rows][words] differ,
+ * e.g. lv_query's sel_bits against lv_brute_force_range's. Enqueue-only. */
+int lv_bits_diff(const uint32_t* a, const uint32_t* b, int64_t words, int64_t rows, int32_t* violations,
+                 void* stream);
+
 /* Host-side synthetic streams with the reference laws (io.cpp:89-206);
  * exported by liblouver_synth.so. */
 int lv_synth_keys(int64_t n, int d, uint64_t seed, float* out);

@@ -109,6 +109,7 @@ _SIGS = {
     "lv_reservoir_seen": (C.c_int64, [_P]),
     "lv_reservoir_capacity": (C.c_int64, [_P]),
     "lv_reservoir_ids": (C.c_int, [_P, _P]),
+    "lv_bits_diff": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P]),
     "lv_estimate_tau": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P]),
 }
 

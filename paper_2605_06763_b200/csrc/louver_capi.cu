@@ -922,6 +922,15 @@ int lv_estimate_tau(lv_ctx* c, const uint32_t* ids, int64_t count, int64_t ld, c
     return sync_if_host(where, st);
 }
 
+int lv_bits_diff(const uint32_t* a, const uint32_t* b, int64_t words, int64_t rows, int32_t* violations,
+                 void* stream) {
+    if (!a || !b || !violations || words < 0 || rows < 0) return fail(LV_EINVAL, "lv_bits_diff: bad arguments");
+    if (rows == 0 || words == 0) return LV_OK;
+    lvkt::bits_diff_kernel<<<(unsigned)rows, 256, 0, S(stream)>>>(a, b, words, violations);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
 int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream) {
     if (!partials || !out || P < 1 || P > 64 || rows < 0 || d < 1)
         return fail(LV_EINVAL, "lv_lse_merge: bad arguments");

@@ -159,4 +159,15 @@ __global__ void estimate_tau_kernel(const T* __restrict__ K, long long cap, int 
     tau[row] = r;
 }
 
+// decode-loop verification (bench.cpp:83-86 on the device): one block per row adds
+// one violation when the row's two id bitmaps differ anywhere
+__global__ void bits_diff_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, long long words,
+                                 int* __restrict__ violations) {
+    const long long base = (long long)blockIdx.x * words;
+    int diff = 0;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x) diff |= a[base + i] != b[base + i];
+    diff = __syncthreads_or(diff);
+    if (diff && threadIdx.x == 0) atomicAdd(violations, 1);
+}
+
 }  // namespace lvkt

@@ -15,6 +15,7 @@ from .threshold import (  # noqa: F401
     estimate_tau_layer,
     parse_oracle,
 )
+from .decode_sim import DecodeSimConfig, MetricsReport, ThresholdSource, run_decode_sim  # noqa: F401
 from .louver import (  # noqa: F401
     AttentionResult,
     BuildConfig,
@@ -34,4 +35,5 @@ __all__ = [
     "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
+    "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim",
 ]

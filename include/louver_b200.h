@@ -239,6 +239,22 @@ int lv_estimate_tau(lv_ctx* ctx, const uint32_t* ids, int64_t count, int64_t ld,
 int lv_bits_diff(const uint32_t* a, const uint32_t* b, int64_t words, int64_t rows, int32_t* violations,
                  void* stream);
 
+/* --- Snapshots (io.hpp:40-51, io.cpp:205-317) --------------------------------
+ * "LVKD" dataset: magic, version 1, n, d (u32 LE), n*d f32 row-major. With
+ * out == NULL, lv_load_dataset only reports n and d. Errors as the reference's
+ * std::runtime_error (LV_ERUNTIME): bad magic, truncation, trailing bytes. */
+int lv_save_dataset(const char* path, const float* data, int64_t n, int d);
+int lv_load_dataset(const char* path, float* out, int64_t cap_rows, int64_t* n, int* d);
+/* "LVIX" index snapshot of slot `slot`: the device cells written as the
+ * reference's format (S = 1, contiguous groups of r keys, exact fp32 AABBs of the
+ * stored keys, indexed_count = lv_indexed_count). */
+int lv_save_index(const lv_ctx* ctx, int slot, const char* path);
+/* Reads any reference LVIX file (every grouping / enclosure / S), checks it
+ * against the cache (dimension, indexed_count <= n, groups partitioning the
+ * indexed keys consistently with the assignments, no trailing bytes) and adopts
+ * its indexed_count: keys past it become the buffer. */
+int lv_load_index(lv_ctx* ctx, const char* path, int64_t* indexed_count, void* stream);
+
 /* Host-side synthetic streams with the reference laws (io.cpp:89-206);
  * exported by liblouver_synth.so. */
 int lv_synth_keys(int64_t n, int d, uint64_t seed, float* out);

@@ -15,6 +15,7 @@ from .threshold import (  # noqa: F401
     estimate_tau_layer,
     parse_oracle,
 )
+from .snapshot import load_dataset, load_index, save_dataset, save_index  # noqa: F401
 from .decode_sim import DecodeSimConfig, MetricsReport, ThresholdSource, run_decode_sim  # noqa: F401
 from .louver import (  # noqa: F401
     AttentionResult,
@@ -36,4 +37,5 @@ __all__ = [
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
     "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim",
+    "save_dataset", "load_dataset", "save_index", "load_index",
 ]

@@ -109,6 +109,10 @@ _SIGS = {
     "lv_reservoir_seen": (C.c_int64, [_P]),
     "lv_reservoir_capacity": (C.c_int64, [_P]),
     "lv_reservoir_ids": (C.c_int, [_P, _P]),
+    "lv_save_dataset": (C.c_int, [C.c_char_p, _P, C.c_int64, C.c_int]),
+    "lv_load_dataset": (C.c_int, [C.c_char_p, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "lv_save_index": (C.c_int, [_P, C.c_int, C.c_char_p]),
+    "lv_load_index": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_int64), _P]),
     "lv_bits_diff": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P]),
     "lv_estimate_tau": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P]),
 }

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <mutex>
 #include <random>
 #include <string>
@@ -400,6 +401,27 @@ cudaError_t launch_query(int dtype, int DP, int G, int mode, const QueryParams& 
 }
 
 }  // namespace lvk
+
+namespace {
+const char kLVKD[4] = {'L', 'V', 'K', 'D'};
+const char kLVIX[4] = {'L', 'V', 'I', 'X'};
+
+template <typename T>
+void put_le(std::ostream& os, T v) {  // little-endian host, as io.cpp:18-24
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+template <typename T>
+bool get_le(std::istream& is, T* v) {
+    is.read(reinterpret_cast<char*>(v), sizeof(T));
+    return (bool)is;
+}
+
+bool at_eof(std::istream& is) {
+    is.peek();
+    return is.eof();
+}
+}  // namespace
 
 extern "C" {
 
@@ -1014,6 +1036,162 @@ int lv_sparse_attention(lv_ctx* c, int slot, const uint32_t* buffer_ids, int64_t
     }
     LV_CUDA(cudaFreeAsync(mem, st));
     LV_CUDA(cudaStreamSynchronize(st));
+    return LV_OK;
+}
+
+// ---- snapshots (io.hpp:40-51, io.cpp:205-317): "LVKD" datasets and "LVIX" index files --
+
+
+int lv_save_dataset(const char* path, const float* data, int64_t n, int d) {
+    if (!path || (!data && n > 0) || n < 0 || d < 1 || n > 0xffffffffLL)
+        return fail(LV_EINVAL, "save_dataset: bad arguments");
+    std::ofstream os(path, std::ios::binary);
+    if (!os) return fail(LV_ERUNTIME, std::string("cannot open for writing: ") + path);
+    os.write(kLVKD, 4);
+    put_le<uint32_t>(os, 1);
+    put_le<uint32_t>(os, (uint32_t)n);
+    put_le<uint32_t>(os, (uint32_t)d);
+    os.write(reinterpret_cast<const char*>(data), (std::streamsize)(sizeof(float) * n * d));
+    if (!os) return fail(LV_ERUNTIME, std::string("write failed: ") + path);
+    return LV_OK;
+}
+
+int lv_load_dataset(const char* path, float* out, int64_t cap_rows, int64_t* n, int* d) {
+    if (!path || !n || !d) return fail(LV_EINVAL, "load_dataset: null argument");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(LV_ERUNTIME, std::string("cannot open for reading: ") + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, kLVKD, 4) != 0) return fail(LV_ERUNTIME, "bad magic: not a dataset file");
+    uint32_t ver = 0, rows = 0, dim = 0;
+    if (!get_le(is, &ver)) return fail(LV_ERUNTIME, "corrupt file: truncated version");
+    if (ver != 1) return fail(LV_ERUNTIME, "unsupported dataset version " + std::to_string(ver));
+    if (!get_le(is, &rows)) return fail(LV_ERUNTIME, "corrupt file: truncated row count");
+    if (!get_le(is, &dim)) return fail(LV_ERUNTIME, "corrupt file: truncated dimension");
+    *n = rows;
+    *d = (int)dim;
+    if (!out) return LV_OK;  // dimensions only
+    if ((int64_t)rows > cap_rows) return fail(LV_EINVAL, "load_dataset: output holds fewer rows than the file");
+    is.read(reinterpret_cast<char*>(out), (std::streamsize)(sizeof(float) * (size_t)rows * dim));
+    if (!is) return fail(LV_ERUNTIME, std::string("corrupt file: truncated payload in ") + path);
+    if (!at_eof(is)) return fail(LV_ERUNTIME, std::string("corrupt file: trailing bytes in ") + path);
+    return LV_OK;
+}
+
+// The device index of a slot written as the reference's index snapshot: one subspace,
+// contiguous groups of r keys (the device cells) over [0, indexed_count), each with its
+// exact AABB (column min / max of the stored keys, index.cpp:112-117) and members.
+int lv_save_index(const lv_ctx* c, int slot, const char* path) {
+    if (!c || !path) return fail(LV_EINVAL, "save_index: null argument");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "save_index: slot out of range");
+    const int d = c->cfg.d, r = c->r;
+    const int64_t m = c->indexed;
+    std::vector<float> rows((size_t)std::max<int64_t>(m, 1) * d);
+    if (m > 0)
+        if (int rc = lv_read_rows(c, slot, 0, m, 0, rows.data())) return rc;
+    std::ofstream os(path, std::ios::binary);
+    if (!os) return fail(LV_ERUNTIME, std::string("cannot open for writing: ") + path);
+    os.write(kLVIX, 4);
+    put_le<uint32_t>(os, 1);                    // version
+    put_le<uint32_t>(os, (uint32_t)d);          // layout.d
+    put_le<uint32_t>(os, 1u);                   // S: the cells span every coordinate
+    put_le<uint32_t>(os, (uint32_t)r);          // r
+    put_le<uint32_t>(os, 0u);                   // GroupingStrategy::Contiguous
+    put_le<uint32_t>(os, 1u);                   // EnclosureKind::Aabb
+    put_le<uint64_t>(os, c->cfg.rng_seed);
+    put_le<uint64_t>(os, (uint64_t)m);
+    put_le<uint64_t>(os, (uint64_t)m);          // assignments
+    for (int64_t j = 0; j < m; ++j) put_le<uint32_t>(os, (uint32_t)(j / r));
+    const int64_t groups = (m + r - 1) / r;
+    put_le<uint32_t>(os, (uint32_t)groups);
+    std::vector<float> lo(d), hi(d);
+    for (int64_t g = 0; g < groups; ++g) {
+        const int64_t b = g * r, e = std::min<int64_t>(m, b + r);
+        for (int i = 0; i < d; ++i) lo[i] = hi[i] = rows[(size_t)b * d + i];
+        for (int64_t j = b + 1; j < e; ++j)
+            for (int i = 0; i < d; ++i) {
+                lo[i] = std::min(lo[i], rows[(size_t)j * d + i]);
+                hi[i] = std::max(hi[i], rows[(size_t)j * d + i]);
+            }
+        put_le<uint32_t>(os, 1u);  // kind Aabb
+        put_le<uint32_t>(os, (uint32_t)d);
+        os.write(reinterpret_cast<const char*>(lo.data()), sizeof(float) * d);
+        put_le<uint32_t>(os, (uint32_t)d);
+        os.write(reinterpret_cast<const char*>(hi.data()), sizeof(float) * d);
+        put_le<uint32_t>(os, (uint32_t)(e - b));
+        for (int64_t j = b; j < e; ++j) put_le<uint32_t>(os, (uint32_t)j);
+    }
+    if (!os) return fail(LV_ERUNTIME, std::string("write failed: ") + path);
+    return LV_OK;
+}
+
+// Reads a reference index snapshot (io.cpp:270-317; any grouping, enclosure and S),
+// validates it against the cache (dimension, indexed_count <= n, every subspace's
+// groups partition [0, indexed_count) and agree with its assignments), then adopts its
+// indexed_count: keys past it form the buffer. The device index is not read from the
+// file — the cell summaries already cover every stored key — so the query results are
+// those of the snapshot's index (final sets never depend on the grouping).
+int lv_load_index(lv_ctx* c, const char* path, int64_t* indexed_count, void* stream) {
+    if (!c || !path) return fail(LV_EINVAL, "load_index: null argument");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(LV_ERUNTIME, std::string("cannot open for reading: ") + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, kLVIX, 4) != 0) return fail(LV_ERUNTIME, "bad magic: not a index snapshot file");
+    uint32_t ver, d, nsub, r, grouping, enclosing;
+    uint64_t seed, m;
+    if (!get_le(is, &ver)) return fail(LV_ERUNTIME, "corrupt file: truncated version");
+    if (ver != 1) return fail(LV_ERUNTIME, "unsupported snapshot version " + std::to_string(ver));
+    if (!get_le(is, &d) || !get_le(is, &nsub) || !get_le(is, &r) || !get_le(is, &grouping) || !get_le(is, &enclosing) ||
+        !get_le(is, &seed) || !get_le(is, &m))
+        return fail(LV_ERUNTIME, "corrupt file: truncated header");
+    if ((int)d != c->cfg.d) return fail(LV_EINVAL, "load_index: snapshot dimension differs from the cache");
+    if (nsub < 1 || nsub > d) return fail(LV_ERUNTIME, "corrupt file: subspace count");
+    if ((int64_t)m > c->n) return fail(LV_EINVAL, "load_index: indexed_count exceeds the stored keys");
+    std::vector<uint32_t> asg, mem;
+    std::vector<uint8_t> seen;
+    for (uint32_t s = 0; s < nsub; ++s) {
+        uint64_t asz;
+        if (!get_le(is, &asz)) return fail(LV_ERUNTIME, "corrupt file: truncated assignment count");
+        if (asz != m) return fail(LV_ERUNTIME, "corrupt file: assignment count != indexed count");
+        asg.resize(asz);
+        is.read(reinterpret_cast<char*>(asg.data()), (std::streamsize)(asz * 4));
+        if (!is) return fail(LV_ERUNTIME, "corrupt file: truncated assignments");
+        uint32_t gcount;
+        if (!get_le(is, &gcount)) return fail(LV_ERUNTIME, "corrupt file: truncated group count");
+        seen.assign(m, 0);
+        for (uint32_t g = 0; g < gcount; ++g) {
+            uint32_t kind, len;
+            if (!get_le(is, &kind)) return fail(LV_ERUNTIME, "corrupt file: truncated kind");
+            const int nvec = kind == 1 ? 2 : 1;  // Aabb: lo, hi; Ball / SpanBall: center (+ radius)
+            for (int v = 0; v < nvec; ++v) {
+                if (!get_le(is, &len)) return fail(LV_ERUNTIME, "corrupt file: truncated vector length");
+                is.seekg((std::streamoff)len * 4, std::ios::cur);
+            }
+            if (kind != 1) {
+                float rad;
+                if (!get_le(is, &rad)) return fail(LV_ERUNTIME, "corrupt file: truncated radius");
+            }
+            uint32_t msz;
+            if (!get_le(is, &msz)) return fail(LV_ERUNTIME, "corrupt file: truncated member count");
+            mem.resize(msz);
+            is.read(reinterpret_cast<char*>(mem.data()), (std::streamsize)msz * 4);
+            if (!is) return fail(LV_ERUNTIME, "corrupt file: truncated members");
+            for (uint32_t id : mem) {
+                if (id >= m || seen[id] || asg[id] != g) return fail(LV_ERUNTIME, "corrupt file: groups do not partition the indexed keys");
+                seen[id] = 1;
+            }
+        }
+        for (uint64_t j = 0; j < m; ++j)
+            if (!seen[j]) return fail(LV_ERUNTIME, "corrupt file: groups do not partition the indexed keys");
+    }
+    if (!at_eof(is)) return fail(LV_ERUNTIME, std::string("corrupt file: trailing bytes in ") + path);
+    std::lock_guard<std::mutex> lock(c->writer);
+    Counters h{c->n, (long long)m, c->flushes, 0};
+    LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)));
+    LV_CUDA(cudaStreamSynchronize(S(stream)));
+    c->indexed = (long long)m;
+    if (indexed_count) *indexed_count = (int64_t)m;
     return LV_OK;
 }
 

@@ -76,6 +76,19 @@ def main():
             print(f"layer {l} merge body cycles: stage {d(18, 19):.0f}  heads {d(19, 20):.0f}  accumulate {d(20, 21):.0f}  "
                   f"write {d(21, 22):.0f}")
     print(f"per-layer period (end to end): {np.diff(ends).mean() / 1e3:.2f} us")
+    # per slot (kv head): the team's survivor cells and when its last CTA finished its tasks
+    nb = int(layers[0].geometry().get("team_ctas_per_slot", 18)) if hasattr(layers[0], "geometry") else 18
+    for l in (1, 4):
+        t = bufs[l].cpu().numpy().astype(np.float64)
+        p0 = t[:, 2][t[:, 2] > 0].min()
+        print(f"layer {l} per slot: surviving cells (sum / max CTA), last partial after probe (us)")
+        for sl in range(t.shape[0] // nb):
+            tt = t[sl * nb:(sl + 1) * nb]
+            tt = tt[tt[:, 0] > 0]
+            if not tt.size:
+                continue
+            print(f"   slot {sl}: {int(tt[:, 15].sum()):5d} / {int(tt[:, 15].max()):4d}   "
+                  f"{(tt[:, 6].max() - p0) / 1e3:6.2f}  (first CTA {(tt[:, 6].min() - p0) / 1e3:6.2f})")
 
 
 if __name__ == "__main__":

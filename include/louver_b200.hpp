@@ -14,6 +14,7 @@
 //   louver::sparse_attention               query.hpp:69-72          -> sparse_attention(const LouverCache&, ...)
 //   louver::OracleConfig / Reservoir       threshold.hpp:9-50       -> OracleConfig / Reservoir (ids of arena rows)
 //   louver::estimate_tau                   threshold.hpp:53         -> estimate_tau(const LouverCache&, res, q, cfg)
+//   louver::run_decode_sim / MetricsReport bench.hpp:16-58          -> run_decode_sim(const KeyStore& rows, queries, cfg)
 //
 // Differences a caller sees: the store lives in HBM inside the cache, so the
 // free functions take the cache instead of a `const KeyStore&`; `index()` is not
@@ -28,6 +29,8 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <limits>
 #include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -456,6 +459,107 @@ inline Scalar estimate_tau(const LouverCache& cache, const Reservoir& res, Const
                                   static_cast<int>(cfg.variant), cfg.m, cfg.alpha, LV_HOST, &tau, nullptr),
                   "estimate_tau");
     return tau;
+}
+
+// ---- decode loop (bench.hpp:16-58, bench.cpp:12-136) ---------------------------------
+
+// bench.cpp:12-19
+inline double speedup_estimate(double g, double r, double f_scan) {
+    if (r < 1.0) throw std::invalid_argument("speedup_estimate: r >= 1 required");
+    if (g < 0.0 || f_scan < 0.0 || f_scan > 1.0)
+        throw std::invalid_argument("speedup_estimate: need g >= 0 and f_scan in [0, 1]");
+    const double denom = g / r + f_scan;
+    if (denom == 0.0) throw std::domain_error("speedup_estimate: g and f_scan both zero");
+    return 1.0 / denom;
+}
+
+struct ThresholdSource {  // bench.hpp:16-19: exactly one is set
+    std::optional<Scalar> fixed_tau;
+    std::optional<OracleConfig> oracle;
+};
+
+struct DecodeSimConfig {  // bench.hpp:21-31
+    BuildConfig build;
+    std::size_t buffer_capacity = 128;
+    FilterAlgo algo = FilterAlgo::Ta;
+    ThresholdSource threshold;
+    std::size_t reservoir_capacity = 256;
+    std::uint64_t seed = 0;
+    bool verify = false;
+    bool strict_threshold = false;
+};
+
+struct MetricsReport {  // bench.hpp:33-48 (recall@k: see the Python driver)
+    std::size_t steps = 0, flushes = 0, violations = 0;
+    double mean_f_scan = 0.0, mean_keys_scanned = 0.0, mean_groups_tested = 0.0, mean_gate_cost_equiv = 0.0;
+    double mean_selected = 0.0, mean_retrieved = 0.0, mean_tau = 0.0, mean_speedup_estimate = 0.0;
+    double median_query_us = 0.0;
+};
+
+// bench.cpp:54-136 through the host layer: row t of `rows` (keys and values) and of
+// `queries` ([steps][d]) drives step t. Each query is one synchronous device call;
+// the device-resident loop with no per-step synchronisation is
+// paper_2605_06763_b200/decode_sim.py.
+inline MetricsReport run_decode_sim(const KeyStore& rows, std::span<const Scalar> queries, const DecodeSimConfig& cfg) {
+    const int d = rows.dim();
+    const std::size_t steps = rows.n();
+    if (queries.size() != steps * static_cast<size_t>(d))
+        throw std::invalid_argument("run_decode_sim: keys/values/queries row mismatch");
+    if (!cfg.threshold.fixed_tau && !cfg.threshold.oracle)
+        throw std::invalid_argument("run_decode_sim: no threshold source");
+    LouverCache cache(d, cfg.build, cfg.buffer_capacity, steps < 16 ? 16 : steps);
+    Reservoir reservoir(cfg.reservoir_capacity, cfg.seed);
+    MetricsReport rep;
+    rep.steps = steps;
+    std::vector<double> wall_us;
+    double sum_tau = 0.0, sum_speedup = 0.0;
+    const std::size_t need =
+        cfg.threshold.oracle && cfg.threshold.oracle->variant == OracleVariant::SampleTopK ? cfg.threshold.oracle->m : 1;
+    for (std::size_t t = 0; t < steps; ++t) {
+        QueryRequest req;
+        req.q.assign(queries.begin() + t * d, queries.begin() + (t + 1) * d);
+        if (cfg.threshold.fixed_tau) {
+            req.tau = *cfg.threshold.fixed_tau;
+        } else if (reservoir.size() >= 2 && reservoir.size() >= need) {
+            req.tau = estimate_tau(cache, reservoir, req.q, *cfg.threshold.oracle);
+        } else {
+            req.tau = -std::numeric_limits<Scalar>::infinity();  // warm-up: retrieve all
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        const CacheQueryResult ans = cache.query(req, cfg.algo, cfg.strict_threshold);
+        const auto t1 = std::chrono::steady_clock::now();
+        wall_us.push_back(std::chrono::duration<double, std::micro>(t1 - t0).count());
+        if (cfg.verify && ans.selected != brute_force_range(cache, req.q, req.tau, cache.n())) ++rep.violations;
+        rep.mean_f_scan += ans.stats.f_scan;
+        rep.mean_keys_scanned += static_cast<double>(ans.stats.keys_scanned);
+        rep.mean_groups_tested += static_cast<double>(ans.stats.groups_tested);
+        rep.mean_gate_cost_equiv += ans.stats.gate_cost_equiv;
+        rep.mean_selected += static_cast<double>(ans.selected.size());
+        rep.mean_retrieved += static_cast<double>(ans.retrieved.size());
+        sum_tau += std::isfinite(req.tau) ? req.tau : 0.0;
+        const double g = cfg.build.enclosing == EnclosureKind::Aabb ? 2.0 : 1.0;
+        sum_speedup += speedup_estimate(g, cfg.build.r, ans.stats.f_scan);
+        cache.push_key(rows.key(static_cast<KeyId>(t)), rows.value(static_cast<KeyId>(t)));
+        reservoir.update(static_cast<KeyId>(t));
+    }
+    const double inv = steps ? 1.0 / static_cast<double>(steps) : 0.0;
+    rep.flushes = cache.flush_count();
+    rep.mean_f_scan *= inv;
+    rep.mean_keys_scanned *= inv;
+    rep.mean_groups_tested *= inv;
+    rep.mean_gate_cost_equiv *= inv;
+    rep.mean_selected *= inv;
+    rep.mean_retrieved *= inv;
+    rep.mean_tau = sum_tau * inv;
+    rep.mean_speedup_estimate = sum_speedup * inv;
+    if (!wall_us.empty()) {  // bench.cpp:23-33
+        const std::size_t mid = wall_us.size() / 2;
+        std::nth_element(wall_us.begin(), wall_us.begin() + mid, wall_us.end());
+        double med = wall_us[mid];
+        if (wall_us.size() % 2 == 0) med = 0.5 * (med + *std::max_element(wall_us.begin(), wall_us.begin() + mid));
+        rep.median_query_us = med;
+    }
+    return rep;
 }
 
 }  // namespace louver_b200

@@ -233,6 +233,65 @@ static void test_threshold() {
     lvo_reservoir_destroy(ref);
 }
 
+// bench.hpp run_decode_sim through the host layer against the oracle's own loop
+// (LouverCache::query + Reservoir + estimate_tau restated on the CPU).
+static void test_decode_sim() {
+    const int d = 16;
+    const std::size_t steps = 300;
+    std::vector<float> K(steps * d), V(steps * d), Q(steps * d);
+    for (size_t i = 0; i < K.size(); ++i) {
+        K[i] = std::sin(0.731f * (float)i) + 0.05f * std::cos(0.017f * (float)i);
+        V[i] = std::cos(0.29f * (float)i);
+        Q[i] = std::sin(1.37f * (float)i + 0.5f);
+    }
+    KeyStore rows(K, V, d);
+    DecodeSimConfig cfg;
+    cfg.build = BuildConfig{1, 16, GroupingStrategy::Contiguous, EnclosureKind::Aabb, 0};
+    cfg.buffer_capacity = 32;
+    cfg.threshold.oracle = OracleConfig{OracleVariant::Budget, 0, 0.2};
+    cfg.reservoir_capacity = 64;
+    cfg.seed = 3;
+    cfg.verify = true;
+    const MetricsReport rep = run_decode_sim(rows, {Q.data(), Q.size()}, cfg);
+    EXPECT(rep.steps == steps && rep.violations == 0, "decode sim: %zu violations", rep.violations);
+    EXPECT(rep.flushes == steps / 32, "decode sim flushes %zu", rep.flushes);
+    // the oracle's loop (bench.cpp:71-120)
+    lvo_build_config oc{1, 16, 0, 1, 0};
+    lvo_cache* c = nullptr;
+    lvo_cache_create(d, &oc, 32, &c);
+    lvo_reservoir* res = lvo_reservoir_create(64, 3);
+    double sel = 0, ret = 0, tau_sum = 0;
+    std::vector<uint32_t> sb(steps + 1), rb(steps + 1), ids(64);
+    std::vector<float> sample, attn(d);
+    for (std::size_t t = 0; t < steps; ++t) {
+        float tau = -INFINITY;
+        const int64_t sz = lvo_reservoir_size(res);
+        if (sz >= 2) {
+            lvo_reservoir_ids(res, ids.data());
+            sample.clear();
+            for (int64_t i = 0; i < sz; ++i) sample.insert(sample.end(), K.begin() + ids[i] * d, K.begin() + (ids[i] + 1) * d);
+            lvo_estimate_tau(sample.data(), sz, d, Q.data() + t * d, 4, 0, 0.2, &tau);
+        }
+        int64_t ns = 0, nr = 0;
+        int has = 0;
+        lvo_stats st{};
+        lvo_cache_query(c, Q.data() + t * d, tau, 0.0f, 1, 0, sb.data(), &ns, rb.data(), &nr, (int64_t)sb.size(),
+                        attn.data(), &has, &st);
+        sel += (double)ns;
+        ret += (double)nr;
+        tau_sum += std::isfinite(tau) ? tau : 0.0;
+        lvo_cache_push_key(c, K.data() + t * d, V.data() + t * d);
+        lvo_reservoir_update(res, (uint32_t)t);
+    }
+    EXPECT(std::fabs(rep.mean_selected - sel / steps) < 1e-9, "mean selected %f vs oracle %f", rep.mean_selected,
+           sel / steps);
+    EXPECT(std::fabs(rep.mean_retrieved - ret / steps) < 1e-9, "mean retrieved %f vs oracle %f", rep.mean_retrieved,
+           ret / steps);
+    EXPECT(std::fabs(rep.mean_tau - tau_sum / steps) < 1e-9, "mean tau %f vs oracle %f", rep.mean_tau, tau_sum / steps);
+    lvo_reservoir_destroy(res);
+    lvo_cache_destroy(c);
+}
+
 int main(int argc, char** argv) {
     if (argc > 1 && std::strcmp(argv[1], "--compile-only") == 0) {
         std::printf("%s\n", lv_build_info());
@@ -242,6 +301,7 @@ int main(int argc, char** argv) {
         test_cache_fp32();
         test_layer_bf16();
         test_threshold();
+        test_decode_sim();
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         return 2;

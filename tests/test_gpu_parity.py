@@ -203,7 +203,16 @@ def taus_at(oracle, K, Q, G, frac):
     return tau
 
 
-def check_layer(torch, oracle, layer, K, V, Q, tau, *, strict=False, indexed=None):
+def exact_attention(kh, vh, q, att):
+    """float64 softmax attention over the attended ids (the exact value both fp32 paths approximate)."""
+    s = (kh[att].astype(np.float64) @ q.astype(np.float64)) / math.sqrt(q.size)
+    w = np.exp(s - s.max())
+    return (w[:, None] * vh[att].astype(np.float64)).sum(0) / w.sum()
+
+
+def check_layer(torch, oracle, layer, K, V, Q, tau, *, strict=False, indexed=None, anchored=False):
+    """anchored: the output bound is relative to exact (float64) attention — REL_TOL, or twice
+    the reference's own fp32 error when its scores are large enough for that to dominate."""
     batch, H_q, d = Q.shape
     G = layer.G
     n = layer.n
@@ -233,7 +242,11 @@ def check_layer(torch, oracle, layer, K, V, Q, tau, *, strict=False, indexed=Non
                 assert cnt[b, hq, 3] == 0 and not outs[b, hq].any()
             else:
                 assert cnt[b, hq, 1] == ow[0].size
-                assert rel_err(outs[b, hq], ow[2]) <= REL_TOL, (b, hq)
+                if anchored:
+                    ex = exact_attention(kh, vh, Q[b, hq], att)
+                    assert rel_err(outs[b, hq], ex) <= max(REL_TOL, 2 * rel_err(ow[2], ex)), (b, hq)
+                else:
+                    assert rel_err(outs[b, hq], ow[2]) <= REL_TOL, (b, hq)
     return cnt
 
 
@@ -251,6 +264,27 @@ def test_layer_query_group_sizes(torch, oracle, G, dtype):
     tau = taus_at(oracle, K, Q, G, 0.10)
     check_layer(torch, oracle, layer, K, V, Q, tau)
     check_layer(torch, oracle, layer, K, V, Q, tau, strict=True)
+
+
+@pytest.mark.parametrize("d", [64, 96, 200, 256])
+def test_layer_query_padded_dims(torch, oracle, d):
+    """Head dimensions the arena pads (d -> DP in {64, 128, 256}): zero columns never
+    change a normative score, the bound or the attention output. Ids bit-exact; the output
+    is anchored to exact attention: at d = 256 this seed's scores reach |s| ~ 3000, where the
+    reference's own fp32 output is ~1e-3 from exact (measured: device 9.3e-4, oracle 1.1e-3)."""
+    layer, K, V, Q = make_layer(torch, oracle, H_kv=2, G=4, batch=2, n=1500, d=d, r=16, seed=300 + d)
+    tau = taus_at(oracle, K, Q, 4, 0.05)
+    check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
+
+
+def test_layer_query_many_cells_per_cta(torch, oracle):
+    """A single slot with a long context: every team CTA lists hundreds of cells (and the
+    list leaves shared memory when it outgrows it), and the tail cell is partial."""
+    layer, K, V, Q = make_layer(torch, oracle, H_kv=1, G=4, batch=1, n=262144 + 77, r=16, seed=41)
+    tau = taus_at(oracle, K, Q, 4, 0.02)
+    # ~5K attended keys: the fp32 paths' summation orders differ by ~2e-4 here, so the
+    # output is anchored to exact attention (ids stay bit-exact)
+    check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
 
 
 def test_layer_iid_queries_and_extreme_taus(torch, oracle):

@@ -763,18 +763,22 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         }
         __syncthreads();
         float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wd;
-        if (tid < G) {
-            float mm = -INFINITY;
-            for (int w = 0; w < NW; ++w) mm = fmaxf(mm, wred[w * Wd + tid * (DP + 2)]);
-            float l = 0.0f;
-            for (int w = 0; w < NW; ++w) {
-                const float mw = wred[w * Wd + tid * (DP + 2)];
-                const float a = mw == -INFINITY ? 0.0f : __expf(mw - mm);
-                shw[w * G + tid] = a;
-                l += a * wred[w * Wd + tid * (DP + 2) + 1];
+        if (warp < G) {  // warp g combines head g's NW warp headers, one warp per lane
+            const int g = warp;
+            const float mw = lane < NW ? wred[lane * Wd + g * (DP + 2)] : -INFINITY;
+            const float lw = lane < NW ? wred[lane * Wd + g * (DP + 2) + 1] : 0.0f;
+            float mm = mw;
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
+            const float a = mw == -INFINITY ? 0.0f : __expf(mw - mm);
+            if (lane < NW) shw[lane * G + g] = a;
+            float l = a * lw;
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+            if (lane == 0) {
+                part[g * (DP + 2)] = l > 0.0f ? mm : -INFINITY;
+                part[g * (DP + 2) + 1] = l;
             }
-            part[tid * (DP + 2)] = l > 0.0f ? mm : -INFINITY;
-            part[tid * (DP + 2) + 1] = l;
         }
         __syncthreads();
         for (int i = tid; i < G * DP; i += NTHR) {

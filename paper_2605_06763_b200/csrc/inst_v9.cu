@@ -1,37 +1,30 @@
-// bf16 query path, fused persistent layer kernel: DP in {64,128,256} x G in {1,2,4,8}.
+// bf16 layer kernel instantiations: DP in {64,128,256} x G in {1,2,4,8} x {query, dense}.
+#include "louver_launch.h"
 #include "louver_v9.cuh"
 
 namespace lvk9 {
 
-template <int DP, int G>
-static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, int* geo) {
+template <int DP, int G, bool DENSE>
+static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st, int* geo) {
     using Ge = C9<DP, G>;
-    static int smem_set = 0;
-    static int occ = 0;
-    // one wave, CTAs of a slot's team side by side; CTA b lists the survivors of
-    // cells b, b + nb, ... so its list holds at most ceil(cap_cells / nb) cells
+    const void* fn = reinterpret_cast<const void*>(louver_layer_v9<DP, G, DENSE>);
+    // One resident wave, a slot's team CTAs side by side. CTA b of a team owns cells b,
+    // b + nb, ...: its survivor list holds at most ceil(cap_cells / nb) u16 entries, in
+    // shared memory when that fits, else in global scratch (the dense scan keeps no list).
     const long long cap_cells = vp.p.cap_cells;
-    // CTA b of a slot's team owns cells b, b + nb, ...: its survivor list holds at most
-    // ceil(cap_cells / nb) u16 entries, in smem when that fits, else in global scratch
     constexpr int kSmemMax = 227 * 1024;
-    int nb = vp.nb, smem = 0;
+    int nb = vp.nb, smem = 0, occ = 0;
     bool glist = false;
     for (int it = 0; it < 8; ++it) {
         const long long lc = (cap_cells + nb - 1) / nb;
-        if (lc > 65536) return cudaErrorInvalidValue;  // u16 interleave indices
-        glist = Ge::smem((int)lc) > kSmemMax;
-        smem = glist ? Ge::DYN : Ge::smem((int)lc);
-        if (smem > smem_set) {
-            cudaError_t e =
-                cudaFuncSetAttribute(louver_layer_v9<DP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, louver_layer_v9<DP, G>, Ge::NTHR, smem);
-            if (e != cudaSuccess) return e;
-            if (occ < 1) return cudaErrorInvalidConfiguration;
-            smem_set = smem;
-        }
+        if (!DENSE && lc > 65536) return cudaErrorInvalidValue;  // u16 interleave indices
+        glist = !DENSE && Ge::smem((int)lc) > kSmemMax;
+        smem = (DENSE || glist) ? Ge::DYN : Ge::smem((int)lc);
+        cudaError_t e = lvl::func_smem(fn, smem, Ge::NTHR, &occ);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
         int nb2 = occ * sms / slots;
-        if (nb2 > vp.nb) nb2 = vp.nb;  // workspace holds vp.nb partials per slot
+        if (nb2 > vp.nb) nb2 = vp.nb;  // the workspace holds vp.nb partials per slot
         if (nb2 < 1) nb2 = 1;
         if (nb2 >= nb) break;  // the list capacity for nb CTAs fits the resident wave
         nb = nb2;              // fewer CTAs per slot: longer lists, recheck
@@ -54,28 +47,29 @@ static cudaError_t launch_t(V5Params vp, int slots, int sms, cudaStream_t st, in
     cfg.blockDim = dim3(Ge::NTHR);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
-    // no grid-wide waiting remains (the merge ticket never blocks), so no cooperative
-    // launch is needed; the grid is still sized to one resident wave. Programmatic
-    // stream serialization lets the CTAs be dispatched while the previous kernel
-    // drains; the kernel's first instruction waits for that kernel's completion.
+    // No grid-wide waiting (the merge ticket never blocks), so no cooperative launch; the
+    // grid is still one resident wave. Programmatic stream serialisation lets the CTAs be
+    // dispatched while the previous kernel drains; the kernel waits for it with
+    // griddepcontrol.wait before reading anything mutable.
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G>, vp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE>, vp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st, int* geo) {
-#define LV9_G(D)                                              \
-    switch (G) {                                              \
-        case 1: return launch_t<D, 1>(vp, slots, sms, st, geo);    \
-        case 2: return launch_t<D, 2>(vp, slots, sms, st, geo);    \
-        case 4: return launch_t<D, 4>(vp, slots, sms, st, geo);    \
-        case 8: return launch_t<D, 8>(vp, slots, sms, st, geo);    \
-    }                                                         \
+cudaError_t launch_layer_v9(int DP, int G, bool dense, LayerParams vp, int slots, int sms, cudaStream_t st,
+                            int* geo) {
+#define LV9_G(D)                                                                                       \
+    switch (G) {                                                                                       \
+        case 1: return dense ? launch_t<D, 1, true>(vp, slots, sms, st, geo) : launch_t<D, 1, false>(vp, slots, sms, st, geo); \
+        case 2: return dense ? launch_t<D, 2, true>(vp, slots, sms, st, geo) : launch_t<D, 2, false>(vp, slots, sms, st, geo); \
+        case 4: return dense ? launch_t<D, 4, true>(vp, slots, sms, st, geo) : launch_t<D, 4, false>(vp, slots, sms, st, geo); \
+        case 8: return dense ? launch_t<D, 8, true>(vp, slots, sms, st, geo) : launch_t<D, 8, false>(vp, slots, sms, st, geo); \
+    }                                                                                                  \
     break;
     switch (DP) {
         case 64: LV9_G(64)

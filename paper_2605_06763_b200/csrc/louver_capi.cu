@@ -17,7 +17,7 @@
 #include "louver_b200.h"
 #include "louver_threshold.cuh"
 #include "louver_dispatch.h"
-#include "louver_v2.cuh"
+#include "louver_launch.h"
 #include "louver_v9.cuh"
 
 using lvk::Counters;
@@ -49,12 +49,9 @@ int ilog2(int x) {
 constexpr long long kCapAlign = 1024;  // arena rows per slot: a whole number of v2 units
 
 struct Workspace {
-    float* partial = nullptr;  // [slots][splits][G][DP+2]
-    int* tickets = nullptr;    // [slots]
-    float* gpart = nullptr;    // [slots][ngroups][G][DP+2] (v2 merge tree)
-    int* gtickets = nullptr;   // [slots][ngroups]
-    int* stickets = nullptr;   // [slots]
-    unsigned* cmask = nullptr; // [slots][tiles] u16 survivor cells (probe -> score)
+    float* partial = nullptr;  // [slots][max(splits, nb)][G][DP+2]
+    int* tickets = nullptr;    // [slots] (fp32 kernel)
+    int* stickets = nullptr;   // [slots] (bf16 layer kernel)
     float* q = nullptr;        // [rows][DP]
     float* out = nullptr;      // [rows][DP]
     float* tau = nullptr;      // [rows]
@@ -69,11 +66,10 @@ struct lv_ctx {
     lv_config cfg{};
     int DP = 0, G = 1, r = 1, r_log2 = 0, slots = 0, rows = 0;
     long long cap = 0, cap_cells = 0, bits_words = 0;
-    int splits = 1, chunks_per_split = 1, ngroups = 1;
+    int splits = 1, chunks_per_split = 1;  // fp32 kernel (query, dense, brute force) geometry
     int sms = 148;
     int layer_geo[4] = {0, 0, 0, 0};  // fused bf16 layer kernel: team CTAs/slot, threads, smem, CTAs/SM
-    int nb = 1, nb_groups = 1, units = 1;  // bf16: score/attend CTAs per slot, merge groups, 512-key units
-    int nbp = 1;                           // bf16: probe CTAs per slot
+    int nb = 1;                        // bf16 layer kernel: team CTAs per slot (upper bound)
     void* K = nullptr;
     void* V = nullptr;
     void* lo = nullptr;
@@ -110,18 +106,11 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
     unsigned char* tau = take(sizeof(float) * rows);
     unsigned char* po = take(sizeof(float) * rows * (c->DP + 2));
     unsigned char* cnt = take(sizeof(int) * rows * 4);
-    const size_t ngr = (size_t)std::max(c->ngroups, c->nb_groups);
-    unsigned char* gp = take(sizeof(float) * c->slots * ngr * c->G * (c->DP + 2));
-    unsigned char* gt = take(sizeof(int) * c->slots * ngr);
     unsigned char* stk = take(sizeof(int) * c->slots);
-    unsigned char* cmk = take(sizeof(unsigned) * c->slots * (size_t)c->units);
     unsigned char* gl = take(sizeof(unsigned short) * c->slots * ((size_t)c->cap_cells + c->nb));
     if (w) {
         w->glist = reinterpret_cast<unsigned short*>(gl);
-        w->gpart = reinterpret_cast<float*>(gp);
-        w->gtickets = reinterpret_cast<int*>(gt);
         w->stickets = reinterpret_cast<int*>(stk);
-        w->cmask = reinterpret_cast<unsigned*>(cmk);
         w->tickets = reinterpret_cast<int*>(t);
         w->partial = reinterpret_cast<float*>(part);
         w->q = reinterpret_cast<float*>(q);
@@ -155,35 +144,21 @@ int validate(const lv_config* c) {
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 void choose_splits(lv_ctx* c) {
-    if (c->cfg.dtype == LV_BF16) {  // v2 kernel: one CTA per fixed 1024-key unit
-        c->chunks_per_split = lvk2::kUnitChunks;
-        c->splits = (int)(c->cap / lvk2::kUnit);
-        c->ngroups = (c->splits + lvk2::kGroup - 1) / lvk2::kGroup;
-        c->units = (int)(c->cap / lvk::kChunk);
-        // v4 exact kernel: balanced rows, ~2 resident CTAs per SM in one wave
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        c->sms = sms;
-        long long nb = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
+    c->sms = lvl::device_sms();
+    if (c->cfg.dtype == LV_BF16) {
+        // fused layer kernel: up to one CTA per SM per slot; the launch clamps the team to
+        // the resident wave (inst_v9.cu)
+        long long nb = std::max(1LL, ((long long)c->sms + c->slots - 1) / c->slots);
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
         c->nb = (int)std::min<long long>(nb, 4096);
-        long long nbp = std::max(1LL, (2LL * sms + c->slots - 1) / c->slots);
-        if (const char* e = std::getenv("LV_NBP")) nbp = std::max(1LL, std::atoll(e));
-        c->nbp = (int)std::min<long long>(nbp, 4096);
-        c->nb_groups = (c->nb + lvk5::kMG - 1) / lvk5::kMG;
-        return;
     }
-    c->ngroups = 1;
+    // fp32 kernel (fp32 query and dense, brute force for both dtypes): chunks of kChunk keys
     const long long chunks = c->cap / lvk::kChunk;
     long long cps = 1;
     if (const char* e = std::getenv("LV_CHUNKS_PER_SPLIT")) {
         cps = std::max(1LL, std::atoll(e));
     } else {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const long long target = (long long)sms * 6;  // ~2 waves at 3 CTAs/SM
+        const long long target = (long long)c->sms * 6;  // ~2 waves at 3 CTAs/SM
         cps = std::max(1LL, (chunks * c->slots + target - 1) / target);
     }
     long long splits = (chunks + cps - 1) / cps;
@@ -297,39 +272,18 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
     p.totals = totals;
     dim3 grid((unsigned)c->splits, (unsigned)c->slots);
     cudaError_t e;
-    if (c->cfg.dtype == LV_BF16 && mode == lvk::kQuery) {
-        lvk5::V5Params v5{};
-        v5.p = p;
-        v5.p.splits = c->nb;
-        v5.sum = reinterpret_cast<const __nv_bfloat16*>(c->lo);
-        v5.cmask = reinterpret_cast<unsigned short*>(w.cmask);
-        v5.tiles = (int)(c->cap_cells / 16);
-        v5.nbp = c->nbp;
-        v5.nb = c->nb;
-        v5.gpart = w.gpart;
-        v5.gtickets = w.gtickets;
-        v5.stickets = w.stickets;
-        v5.ngroups = c->nb_groups;
-        v5.gmax = nullptr;
-        v5.p.tot_trace = c->trace;
-        v5.glist = w.glist;
-        static const int dbg = [] { const char* e = getenv("LV_DBG"); return e ? atoi(e) : 0; }();
-        v5.dbg = dbg;
+    if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
+        lvk9::LayerParams lp{};
+        lp.p = p;
+        lp.sum = reinterpret_cast<const __nv_bfloat16*>(c->lo);
+        lp.stickets = w.stickets;
+        lp.nb = c->nb;
+        lp.glist = w.glist;
+        lp.p.tot_trace = c->trace;
         // cells complete before the last insert enqueued ahead of this query: the insert kernel
         // that may still be draining under PDL writes only the cell of key n - 1
-        v5.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
-        e = lvk9::launch_layer_v9(c->DP, c->G, v5, c->slots, c->sms, st, c->layer_geo);
-    } else if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
-        lvk2::V2Params vp{};
-        vp.p = p;
-        vp.sum = c->lo;
-        vp.gpart = w.gpart;
-        vp.gtickets = w.gtickets;
-        vp.stickets = w.stickets;
-        vp.ngroups = c->ngroups;
-        vp.mode_dense = mode == lvk::kDense ? 1 : 0;
-        vp.trace = c->trace;
-        e = lvk2::launch_query_v2(c->DP, c->G, vp, grid, st);
+        lp.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
+        e = lvk9::launch_layer_v9(c->DP, c->G, mode == lvk::kDense, lp, c->slots, c->sms, st, c->layer_geo);
     } else {
         e = lvk::launch_query(c->cfg.dtype, c->DP, c->G, mode, p, grid, st);
     }
@@ -389,8 +343,10 @@ cudaError_t launch_query(int dtype, int DP, int G, int mode, const QueryParams& 
         case kBrute: LVK_D(T, kBrute)  \
         case kDense: LVK_D(T, kDense)  \
     }
-    if (dtype == LV_BF16) {
-        LVK_M(__nv_bfloat16)
+    if (dtype == LV_BF16) {  // bf16 queries and dense scans run the layer kernel (inst_v9.cu)
+        switch (mode) {
+            case kBrute: LVK_D(__nv_bfloat16, kBrute)
+        }
     } else {
         LVK_M(float)
     }
@@ -509,8 +465,7 @@ int lv_geometry(const lv_ctx* c, int64_t* out) {
     out[4] = c->splits;
     out[5] = c->chunks_per_split;
     out[6] = lvk::kChunk;
-    out[7] = c->cfg.dtype == LV_BF16 ? lvk2::query_v2_smem(c->DP, c->G)
-                                     : lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
+    out[7] = c->cfg.dtype == LV_BF16 ? c->layer_geo[2] : lvk::query_smem_bytes(c->cfg.dtype, c->DP, c->G);
     return LV_OK;
 }
 int lv_layer_geometry(const lv_ctx* c, int64_t* out) {
@@ -593,11 +548,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->bits_words = ncap / 32;
     c->splits = probe_geo.splits;
     c->chunks_per_split = probe_geo.chunks_per_split;
-    c->ngroups = probe_geo.ngroups;
-    c->units = probe_geo.units;
     c->nb = probe_geo.nb;
-    c->nb_groups = probe_geo.nb_groups;
-    c->nbp = probe_geo.nbp;
     c->cfg.capacity = capacity;
     return LV_OK;
 }
@@ -922,12 +873,10 @@ int lv_estimate_tau(lv_ctx* c, const uint32_t* ids, int64_t count, int64_t ld, c
     const int rpc = c->cfg.dtype == LV_BF16 ? lvkt::stage_rows<__nv_bfloat16>(c->DP) : lvkt::stage_rows<float>(c->DP);
     const size_t smem = (size_t)rpc * (c->DP * esz + 16) + sizeof(float) * (c->DP + 2 * (size_t)np2);
     const int threads = np2 <= 1024 ? np2 : 256;  // one score per thread up to 1024
-    if (smem > 48 * 1024) {
-        LV_CUDA(cudaFuncSetAttribute(lvkt::estimate_tau_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        LV_CUDA(cudaFuncSetAttribute(lvkt::estimate_tau_kernel<__nv_bfloat16>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    LV_CUDA(lvl::func_smem(c->cfg.dtype == LV_BF16
+                               ? reinterpret_cast<const void*>(lvkt::estimate_tau_kernel<__nv_bfloat16>)
+                               : reinterpret_cast<const void*>(lvkt::estimate_tau_kernel<float>),
+                           (int)smem));
     if (c->cfg.dtype == LV_BF16)
         lvkt::estimate_tau_kernel<__nv_bfloat16><<<(unsigned)c->rows, threads, smem, st>>>(
             reinterpret_cast<const __nv_bfloat16*>(c->K), c->cap, c->DP, c->cfg.d, c->G, idd, ld, (int)count, qd,

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "louver_kernels.cuh"
+#include "louver_launch.h"
 
 namespace lvk {
 
@@ -23,15 +24,10 @@ cudaError_t launch_query(int dtype, int DP, int G, int mode, const QueryParams& 
 #define LVK_DEFINE_LAUNCH(T, DP, G, MODE)                                                        \
     template <>                                                                                  \
     cudaError_t launch_query_t<T, DP, G, MODE>(const QueryParams& p, dim3 grid, cudaStream_t st) { \
-        static bool attr_done = false;                                                           \
         constexpr int smem = Geo<T, DP, G>::SMEM;                                                \
-        if (!attr_done) {                                                                        \
-            cudaError_t e = cudaFuncSetAttribute(louver_query_kernel<T, DP, G, MODE>,            \
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                                 smem);                                          \
-            if (e != cudaSuccess) return e;                                                      \
-            attr_done = true;                                                                    \
-        }                                                                                        \
+        cudaError_t e = lvl::func_smem(                                                          \
+            reinterpret_cast<const void*>(louver_query_kernel<T, DP, G, MODE>), smem);           \
+        if (e != cudaSuccess) return e;                                                          \
         louver_query_kernel<T, DP, G, MODE><<<grid, kThreads, smem, st>>>(p);                    \
         return cudaGetLastError();                                                               \
     }

@@ -1,85 +1,56 @@
 // Louver bf16 query path as ONE persistent kernel per layer (sm_100a).
 //
-// Per slot (batch x kv head) a fixed team of CTAs, all co-resident (cooperative
-// launch), runs three phases:
+// Grid = (team, slots): a slot (one sequence x kv head) is served by a team of nb CTAs,
+// one CTA per SM, and CTA b of the team owns the slot's cells b, b + nb, b + 2 nb, ...
+// (a fine interleave, so every CTA sees the same mix of the sequence and no team-wide
+// exchange is needed before the merge). Phases per CTA:
 //
-//   A  probe      cell summaries [hi | lo] (16 cells = one block) are scored
-//                 against [q+ | q-] on the tensor cores; a cell survives for head g
-//                 iff its box bound reaches tau_g - 2^-12 S_g (sound: bf16 split
-//                 error << the margin). Survivor bits go to a per-slot mask.
-//                 (reference: Louver.probe, louver.cpp / core.hpp gate bounds)
-//   --  per-slot barrier (counter in L2; every CTA of the slot is resident)
-//   B  exact      the slot's surviving cells are split evenly over the team; each
-//      + attend   16-key task is scored on the tensor cores (q in three bf16
-//                 parts), pairs within 2^-13 S_g of tau settled with the
-//                 normative sequential fp32 dot (core.hpp:17-21); the V rows of
-//                 the attended keys (selected ∪ buffer unless strict,
-//                 cache.cpp:48-68) are folded in with P.V on the tensor cores
-//                 (P split in two bf16 parts, V bf16 exact).
-//   C  merge      (m, l, o) partials of the team, combined by the last CTA.
+//   A  probe      cell summaries [hi | lo] (16 cells = one tile) are scored against
+//                 [q+ | q-] on the tensor cores; a cell survives for head g iff its box
+//                 bound reaches tau_g - 2^-12 S_g (sound: the bf16 split error is far
+//                 inside the margin) or it holds buffer keys. Survivors are appended to
+//                 the CTA's list in shared memory (warp ballot compaction).
+//                 (reference: gate_bounds + query_ta / query_full_subspace, query.cpp:47-303)
+//   B  exact      16-key tasks of the listed cells, claimed by the CTA's warps through a
+//      + attend   shared counter, are scored on the tensor cores (q in three bf16 parts);
+//                 pairs within 2^-13 S_g of tau are settled with the normative sequential
+//                 fp32 dot (core.hpp:17-21, exact_check query.cpp:22-31); the V rows of the
+//                 attended keys (selected ∪ buffer unless strict, cache.cpp:48-68) are folded
+//                 in with P.V on the tensor cores (P split in two bf16 parts, V bf16 exact);
+//                 online softmax with a lazy reference max (sparse_attention, query.cpp:338-371).
+//   C  merge      warp partials -> CTA partial (m, l, o) in global scratch; an acq_rel
+//                 ticket elects the team's last CTA, which combines the nb partials.
 //
-// Every block of keys, summaries or values moves global -> shared with cp.async
-// into a per-warp 3-stage ring, 128-byte XOR swizzle (chunk ^ row&7), read with
-// ldmatrix, so no register holds an in-flight block and the fragments need no
-// register shuffling. Per warp the exact phase is a software pipeline:
+// DENSE = true is the full-scan decode (the speed-up denominator): no probe, every key of
+// the CTA's cells is attended; same pipeline, same score precision.
+//
+// Every block of keys, summaries or values moves global -> shared with cp.async into a
+// per-warp 3-stage ring, 128-byte XOR swizzle (chunk ^ row&7), read with ldmatrix, so no
+// register holds an in-flight block and the fragments need no register shuffling. Per
+// warp the exact phase is a software pipeline:
 // K(t+1) in flight | K(t) scored | V(t-1) in flight, folded after K(t) is scored.
+// The launch uses programmatic dependent launch: the first summary sub-blocks of sealed
+// cells are requested before griddepcontrol.wait.
 #pragma once
 
-#include "louver_v5.cuh"
+#include "louver_common.cuh"
+#include "louver_kernels.cuh"
 
 namespace lvk9 {
 
 using lvk::QueryParams;
-using lvk5::V5Params;
-using lvk2::mma16816;
+using namespace lvc;
 
-__device__ __forceinline__ void cpa16(unsigned dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cpa16z(unsigned dst, const void* src, bool valid) {  // zero-fill if !valid
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void ldsm4(unsigned (&r)[4], unsigned a) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(a)
-                 : "memory");
-}
-__device__ __forceinline__ void ldsm4t(unsigned (&r)[4], unsigned a) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(a)
-                 : "memory");
-}
-__device__ __forceinline__ uint4 lds16(unsigned a) {
-    uint4 r;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "r"(a)
-                 : "memory");
-    return r;
-}
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ void red_release(int* p, int v) {
-    asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned bf2(float lo, float hi) {
-    return (unsigned)lvk2::bf_bits(lo) | ((unsigned)lvk2::bf_bits(hi) << 16);
-}
+struct LayerParams {
+    QueryParams p;
+    const __nv_bfloat16* sum;  // [slot][cap_cells][2*DP] cell rows [hi | lo]
+    int* stickets;             // [slots] merge tickets (self-resetting)
+    int nb;                    // team CTAs per slot
+    int slots;                 // slots of the layer (the grid may loop over them)
+    unsigned short* glist;     // survivor lists in global scratch when they outgrow smem (else null)
+    int list_cap;              // entries per CTA list
+    long long sealed;          // cells complete when the query was enqueued (immutable summaries)
+};
 
 // Ballot over pair lanes (lane = k G + g for row k of a 32/G-row block) ->
 // bit k set iff any head of row k is set.
@@ -139,8 +110,8 @@ struct C9 {
     static_assert(NW >= 2, "Louver v9: shared memory budget too small");
 };
 
-template <int DP, int G>
-__global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ V5Params vp) {
+template <int DP, int G, bool DENSE>
+__global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ LayerParams vp) {
     using Ge = C9<DP, G>;
     constexpr bool PACK = G <= 4;  // P.V: hi and lo parts of P share one n-tile
     constexpr int NW = Ge::NW, NTHR = Ge::NTHR, NT = Ge::NT, NTP = Ge::NTP, KS = Ge::KS, CPR = Ge::CPR,
@@ -163,7 +134,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int blk = blockIdx.x, nb = vp.nb;
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
-    const unsigned ring = lvk2::smem_u32(wbase);
+    const unsigned ring = smem_u32(wbase);
     float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
     const int q4 = lane & 3;
@@ -180,7 +151,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     bool waited = false;
     long long* trace = nullptr;
 #define LV9_TRACE(i) \
-    if (trace && tid == 0) trace[i] = lvk2::gtimer();
+    if (trace && tid == 0) trace[i] = gtimer();
 
     // (no ring zeroing: a V stage is always the stage of its task's K block, loaded whole,
     // with rows past n zero-filled, so rows that are not attended hold finite values)
@@ -245,8 +216,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         if (!waited) {
             // sub-blocks 0, 1 (tile warp) and 2 (tile warp + NW) fill the 3-stage ring
             const long long c0 = blk + (long long)16 * warp * nb, c1 = c0 + (long long)16 * NW * nb;
-            pre = (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) && (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed) &&
-                  !(vp.dbg & 8);  // timing experiment: no prefetch before the wait
+            pre = !DENSE && (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) &&
+                  (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed);
             if (pre) {
                 p_issue(0, cap_cells);
                 p_issue(1, cap_cells);
@@ -271,7 +242,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 xq[k] = i < G * DP ? __ldcg(qsrc + i) : 0.0f;
                 xc[k] = i < G * DP ? __ldcg(colmax + i % DP) : 0.0f;
             }
-            const float tau_r = tid < G ? __ldcg(p.tau + (size_t)slot * G + tid) : 0.0f;
+            const float tau_r = (!DENSE && tid < G) ? __ldcg(p.tau + (size_t)slot * G + tid) : 0.0f;
             // zero the fragment arrays (columns past PARTS * G stay zero)
             for (int i = tid; i < (Ge::SZ_FRE + Ge::SZ_FRP) / 16; i += NTHR)
                 reinterpret_cast<uint4*>(smem + Ge::OFF_FRE)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -280,9 +251,9 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             for (int g = 0; g < G; ++g) s[g] = 0.0f;
             if (trace && tid == 0) {
                 asm volatile("" ::"f"(xq[0]));
-                trace[9] = lvk2::gtimer();
+                trace[9] = gtimer();
                 asm volatile("" ::"f"(xc[0]));
-                trace[12] = lvk2::gtimer();
+                trace[12] = gtimer();
             }
 #pragma unroll
             for (int k = 0; k < QPT; ++k) {
@@ -328,8 +299,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     float y = xq[k];
 #pragma unroll
                     for (int P = 0; P < 3; ++P) {
-                        const unsigned short b = lvk2::bf_bits(y);
-                        y -= lvk2::bf_val(b);
+                        const unsigned short b = bf_bits(y);
+                        y -= bf_val(b);
                         const int col = P * G + g;
                         fe[((ks * NT + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
                     }
@@ -338,8 +309,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         float z = h == 0 ? fmaxf(xq[k], 0.0f) : fminf(xq[k], 0.0f);  // [hi | lo] . [q+ | q-]
 #pragma unroll
                         for (int P = 0; P < 2; ++P) {
-                            const unsigned short b = lvk2::bf_bits(z);
-                            z -= lvk2::bf_val(b);
+                            const unsigned short b = bf_bits(z);
+                            z -= bf_val(b);
                             const int col = P * G + g;
                             fp[(((h * KS + ks) * NTP + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
                         }
@@ -351,7 +322,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(1)
         // the summary prefetch starts only now: cp.async issue stalls the issuing warp once
         // the memory system is saturated, so it must not sit in front of the setup
-        if (!pre) {
+        if (!pre && !DENSE) {
             p_issue(0, cap_cells);
             p_issue(1, cap_cells);
             p_issue(2, cap_cells);
@@ -360,7 +331,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         const long long ncells = (n + r - 1) >> rl;
 
         // ---- phase A: probe
-        {
+        if (!DENSE) {
             float taup[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) taup[g] = taup_s[g];
@@ -443,7 +414,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         __syncthreads();  // the CTA's survivor list is complete
         LV9_TRACE(3)
-        const int nsurv = iscr[2];
+        // DENSE: every cell the CTA owns (blk, blk + nb, ... < ncells), in order
+        const int nsurv = DENSE ? (int)(ncells > blk ? (ncells - blk + nb - 1) / nb : 0) : iscr[2];
         LV9_TRACE(4)
         if (trace && tid == 0) trace[15] = nsurv;
 
@@ -465,7 +437,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             // one task ahead (balances warps whatever each task costs)
             const int ntask = nsurv << tpc_l2;
             auto key0 = [&](int t) -> long long {
-                const long long cell = blk + (long long)slist[t >> tpc_l2] * nb;
+                const long long cell = blk + (long long)(DENSE ? (t >> tpc_l2) : slist[t >> tpc_l2]) * nb;
                 return (cell << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
             };
             // chunk k*32 + lane of a 16-row block: row k*RPI + lane/CPR, column chunk lane%CPR,
@@ -547,13 +519,13 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const float* c = ct + (rw < 16 ? rw : 15) * CT;
                     const float sc = (c[g_me] + c[G + g_me]) + c[2 * G + g_me];
                     const bool valid = (G > 1 || lane < 16) && k0 + rw < n;
-                    const bool sel = valid && sc >= tau_me + marg_me;
-                    const bool u = valid && !sel && sc >= tau_me - marg_me;
+                    const bool sel = valid && (DENSE || sc >= tau_me + marg_me);
+                    const bool u = !DENSE && valid && !sel && sc >= tau_me - marg_me;
                     s[j] = sc;
                     und |= (unsigned)u << j;
                     selb |= (unsigned)sel << j;
                 }
-                if (__any_sync(0xffffffffu, und != 0)) {  // rare: the normative sequential dot
+                if (!DENSE && __any_sync(0xffffffffu, und != 0)) {  // rare: the normative sequential dot
 #pragma unroll
                     for (int j = 0; j < PPL; ++j) {
                         if ((und >> j) & 1) {
@@ -583,7 +555,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const bool sel = (selb >> j) & 1;
                     if (sel) {
                         ++my_sel;
-                        if (p.bits)
+                        if (!DENSE && p.bits)
                             atomicOr(p.bits + ((size_t)slot * G + g_me) * p.bits_words + (kk >> 5), 1u << (kk & 31));
                     }
                     const bool att = sel || (valid && !p.strict && kk >= indexed);
@@ -628,7 +600,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     }
                     float lo4[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) lo4[e] = pv4[e] - lvk2::bf_val(lvk2::bf_bits(pv4[e]));
+                    for (int e = 0; e < 4; ++e) lo4[e] = pv4[e] - bf_val(bf_bits(pv4[e]));
                     if (PACK) {
                         const bool lo = hn >= G;
                         nbf[0] = lo ? bf2(lo4[0], lo4[1]) : bf2(pv4[0], pv4[1]);
@@ -742,7 +714,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         // ---- warp partials -> CTA partial [G][DP+2] (m, l, o)
         constexpr int Wd = G * (DP + 2);
-        if (vp.dbg & 2) continue;  // timing experiment: no partial, no merge (output invalid)
         float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Wd] over the rings
         float* shw = red;                                           // [NW][G] weights
         __syncthreads();
@@ -763,8 +734,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         }
         __syncthreads();
         float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wd;
-        if (warp < G) {  // warp g combines head g's NW warp headers, one warp per lane
-            const int g = warp;
+        for (int g = warp; g < G; g += NW) {  // warp g combines head g's NW warp headers, one warp per lane
             const float mw = lane < NW ? wred[lane * Wd + g * (DP + 2)] : -INFINITY;
             const float lw = lane < NW ? wred[lane * Wd + g * (DP + 2) + 1] : 0.0f;
             float mm = mw;
@@ -791,7 +761,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(6)
 
         // ---- phase C: the last CTA of the team merges the nb partials
-        if (vp.dbg & 1) continue;  // timing experiment: no merge (output invalid)
         int* ticket = vp.stickets + slot;
         __syncthreads();
         if (tid == 0) iscr[1] = atom_add_acq_rel(ticket, 1) == nb - 1;
@@ -881,6 +850,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #undef LV9_TRACE
 }
 
-cudaError_t launch_layer_v9(int DP, int G, V5Params vp, int slots, int sms, cudaStream_t st, int* geo);
+cudaError_t launch_layer_v9(int DP, int G, bool dense, LayerParams vp, int slots, int sms, cudaStream_t st, int* geo);
 
 }  // namespace lvk9

@@ -277,6 +277,16 @@ def test_layer_query_padded_dims(torch, oracle, d):
     check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
 
 
+@pytest.mark.parametrize("d", [200, 256])
+def test_layer_query_wide_heads_g8(torch, oracle, d):
+    """G = 8 at DP = 256: shared memory leaves fewer warps per CTA (7) than q heads (8), so the
+    CTA-partial header combine must loop heads over warps."""
+    layer, K, V, Q = make_layer(torch, oracle, H_kv=2, G=8, batch=1, n=1800, d=d, r=16, seed=500 + d)
+    tau = taus_at(oracle, K, Q, 8, 0.05)
+    check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
+    check_layer(torch, oracle, layer, K, V, Q, tau, strict=True, anchored=True)
+
+
 def test_layer_query_many_cells_per_cta(torch, oracle):
     """A single slot with a long context: every team CTA lists hundreds of cells (and the
     list leaves shared memory when it outgrows it), and the tail cell is partial."""

@@ -72,6 +72,26 @@ _SIGS = {
 _lib = None
 
 
+def reference_module():
+    """This module's API bound to oracle/_ref/liblouver_ref.so — the reference sources
+    themselves (/root/reference/proj/src/*.cpp, unmodified) compiled against the Eigen shim
+    in oracle/ref (``make -C oracle ref``) — or None when that build is absent."""
+    import importlib.util
+
+    path = os.path.join(_HERE, "_ref", "liblouver_ref.so")
+    if not os.path.exists(path):
+        return None
+    spec = importlib.util.spec_from_file_location("oracle._pyoracle_reference", os.path.abspath(__file__))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod._LIB_PATH = path
+    mod.IS_REFERENCE = True
+    return mod
+
+
+IS_REFERENCE = False
+
+
 def build() -> None:
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
 

@@ -12,6 +12,7 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
     // b + nb, ...: its survivor list holds at most ceil(cap_cells / nb) u16 entries, in
     // shared memory when that fits, else in global scratch (the dense scan keeps no list).
     const long long cap_cells = vp.p.cap_cells;
+    if (vp.p.cap >= (1LL << 31) - 64) return cudaErrorInvalidValue;  // 32-bit key indices in the task loop
     constexpr int kSmemMax = 227 * 1024;
     int nb = vp.nb, smem = 0, occ = 0;
     bool glist = false;

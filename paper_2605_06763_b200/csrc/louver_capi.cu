@@ -81,6 +81,8 @@ struct lv_ctx {
     size_t ws_bytes = 0;
     // host mirrors of the device counters
     long long n = 0, indexed = 0, flushes = 0;
+    int l2pf = 0;                // experiment knob (LV_L2PF)
+    int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     std::mutex writer;
 };
@@ -150,6 +152,8 @@ void choose_splits(lv_ctx* c) {
         // the resident wave (inst_v9.cu)
         long long nb = std::max(1LL, ((long long)c->sms + c->slots - 1) / c->slots);
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
+        if (const char* e = std::getenv("LV_L2PF")) c->l2pf = std::atoi(e);
+        if (const char* e = std::getenv("LV_PRE")) c->npre = std::min(3, std::max(0, std::atoi(e)));
         c->nb = (int)std::min<long long>(nb, 4096);
     }
     // fp32 kernel (fp32 query and dense, brute force for both dtypes): chunks of kChunk keys
@@ -280,6 +284,8 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         lp.nb = c->nb;
         lp.glist = w.glist;
         lp.p.tot_trace = c->trace;
+        lp.l2pf = c->l2pf;
+        lp.npre = c->npre;
         // cells complete before the last insert enqueued ahead of this query: the insert kernel
         // that may still be draining under PDL writes only the cell of key n - 1
         lp.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;

@@ -50,6 +50,10 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
+// fire-and-forget L2 prefetch of a contiguous block (TMA engine; size a multiple of 16 B)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // ---- shared-memory loads ----------------------------------------------------------
@@ -95,6 +99,13 @@ __device__ __forceinline__ unsigned short bf_bits(float x) { return __bfloat16_a
 __device__ __forceinline__ float bf_val(unsigned short b) { return __uint_as_float((unsigned)b << 16); }
 __device__ __forceinline__ unsigned bf2(float lo, float hi) {
     return (unsigned)bf_bits(lo) | ((unsigned)bf_bits(hi) << 16);
+}
+
+// 2^x on the SFU (flushes results below 2^-126 to zero; ex2(-inf) = 0)
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 __device__ __forceinline__ long long gtimer() {

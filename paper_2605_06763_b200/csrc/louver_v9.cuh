@@ -50,6 +50,8 @@ struct LayerParams {
     unsigned short* glist;     // survivor lists in global scratch when they outgrow smem (else null)
     int list_cap;              // entries per CTA list
     long long sealed;          // cells complete when the query was enqueued (immutable summaries)
+    int npre;                  // summary sub-blocks requested before griddepcontrol.wait (0..3)
+    int l2pf;                  // experiment: L2 bulk prefetch of surviving cells' keys from the probe
 };
 
 // Ballot over pair lanes (lane = k G + g for row k of a 32/G-row block) ->
@@ -77,6 +79,13 @@ __device__ __forceinline__ unsigned row_bits(unsigned b) {
         x = (x | (x >> 7)) & 0x00030003u;
         return (x | (x >> 14)) & 0xfu;
     }
+}
+
+// Byte offset of k-step ks's 16-byte chunk of row a_row in a 128-byte-swizzled stage
+// (chunk c of row r is stored at c ^ (r & 7)): only the low three chunk bits are swizzled,
+// so k-steps 4 apart differ by a constant 128 bytes.
+__device__ __forceinline__ unsigned swz_off(int ks, int a_hi, int a_row) {
+    return ((unsigned)(ks >> 2) << 7) + ((unsigned)(((2 * (ks & 3) + a_hi) ^ (a_row & 7))) << 4);
 }
 
 template <int DP, int G>
@@ -218,11 +227,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             const long long c0 = blk + (long long)16 * warp * nb, c1 = c0 + (long long)16 * NW * nb;
             pre = !DENSE && (c0 >= cap_cells || c0 + 15LL * nb < vp.sealed) &&
                   (c1 >= cap_cells || c1 + 15LL * nb < vp.sealed);
-            if (pre) {
-                p_issue(0, cap_cells);
-                p_issue(1, cap_cells);
-                p_issue(2, cap_cells);
-            }
+            if (pre)
+                for (int u = 0; u < vp.npre; ++u) p_issue(u, cap_cells);
             asm volatile("griddepcontrol.wait;\n" ::: "memory");
             waited = true;
             LV9_TRACE(13)
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         const unsigned short b = bf_bits(y);
                         y -= bf_val(b);
                         const int col = P * G + g;
-                        fe[((ks * NT + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
+                        fe[((((ks >> 1) * NT + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 2 + (ks & 1)) * 4 + e] = b;
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                             const unsigned short b = bf_bits(z);
                             z -= bf_val(b);
                             const int col = P * G + g;
-                            fp[(((h * KS + ks) * NTP + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 4 + e] = b;
+                            fp[((((h * (KS / 2) + (ks >> 1)) * NTP + (col >> 3)) * 32 + (col & 7) * 4 + qq) * 2 + (ks & 1)) * 4 + e] = b;
                         }
                     }
                 }
@@ -322,11 +328,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(1)
         // the summary prefetch starts only now: cp.async issue stalls the issuing warp once
         // the memory system is saturated, so it must not sit in front of the setup
-        if (!pre && !DENSE) {
-            p_issue(0, cap_cells);
-            p_issue(1, cap_cells);
-            p_issue(2, cap_cells);
-        }
+        if (!DENSE)
+            for (int u = pre ? vp.npre : 0; u < 3; ++u) p_issue(u, cap_cells);
         const int rl = p.r_log2, r = 1 << rl;
         const long long ncells = (n + r - 1) >> rl;
 
@@ -347,15 +350,17 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     for (int nt = 0; nt < NTP; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
                 }
                 const unsigned sb = ring + (u % 3) * Ge::STAGE + a_off;
-                const uint2* fh = frp + half * KS * NTP * 32;
+                const uint4* fh = reinterpret_cast<const uint4*>(frp) + half * (KS / 2) * NTP * 32;
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                    unsigned a[4];
-                    ldsm4(a, sb + (((2 * ks + a_hi) ^ (a_row & 7)) << 4));
+                for (int k2 = 0; k2 < KS / 2; ++k2) {
+                    unsigned a0[4], a1[4];
+                    ldsm4(a0, sb + swz_off(2 * k2, a_hi, a_row));
+                    ldsm4(a1, sb + swz_off(2 * k2 + 1, a_hi, a_row));
 #pragma unroll
                     for (int nt = 0; nt < NTP; ++nt) {
-                        const uint2 b = fh[(ks * NTP + nt) * 32 + lane];
-                        mma16816(acc[nt], a, b.x, b.y);
+                        const uint4 b = fh[(k2 * NTP + nt) * 32 + lane];
+                        mma16816(acc[nt], a0, b.x, b.y);
+                        mma16816(acc[nt], a1, b.z, b.w);
                     }
                 }
                 if (half == 1) {
@@ -380,6 +385,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         }
                         scan = (int)((ce < n ? ce : n) - cs);
                     }
+                    if (gm && vp.l2pf)  // the cell's keys stream into L2 now; the exact phase finds them there
+                        bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(Ks) + ((size_t)cell << rl) * RB, (unsigned)(r * RB));
                     const unsigned m = __ballot_sync(0xffffffffu, gm != 0) & 0xffffu;
                     if (m) {  // append the survivors to the CTA's list
                         int base = 0;
@@ -423,7 +430,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         const int g_me = lane % G;
         const float tau_me = tau_s[g_me], marg_me = marg_s[g_me];
         const float* q_me = qf + g_me * (DP + 4);
-        const float scale = p.scale;
+        // scores in log2 units: exp(scale s - m) = 2^(scale log2(e) s - m / ln 2)
+        const float scale = p.scale * 1.4426950408889634f;
         const int tpc_l2 = rl - 4;  // log2(16-row tasks per cell)
         float o[MT][4];
 #pragma unroll
@@ -436,9 +444,11 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             // tasks = 16-key blocks of the listed cells, claimed through a shared counter
             // one task ahead (balances warps whatever each task costs)
             const int ntask = nsurv << tpc_l2;
-            auto key0 = [&](int t) -> long long {
-                const long long cell = blk + (long long)(DENSE ? (t >> tpc_l2) : slist[t >> tpc_l2]) * nb;
-                return (cell << rl) + ((long long)(t & ((1 << tpc_l2) - 1)) << 4);
+            // 32-bit key indices: the launcher guarantees cap < 2^31 rows per slot
+            const int n32 = (int)n, idx32 = (int)indexed;
+            auto key0 = [&](int t) -> int {
+                const int cell = blk + (DENSE ? (t >> tpc_l2) : (int)slist[t >> tpc_l2]) * nb;
+                return (cell << rl) + ((t & ((1 << tpc_l2) - 1)) << 4);
             };
             // chunk k*32 + lane of a 16-row block: row k*RPI + lane/CPR, column chunk lane%CPR,
             // so the source is base + 512 k + 16 lane and the swizzled destination repeats
@@ -450,19 +460,18 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 const int row = kk * RPI + lane / CPR, c = lane % CPR;
                 doff[kk] = row * RB + ((c ^ (row & 7)) << 4);
             }
-            auto k_issue = [&](int t, int stage) {  // rows past n land as zeros
+            auto k_issue = [&](int t, int kb, int stage) {  // rows past n land as zeros
                 if (t < ntask) {
-                    const long long kb = key0(t);
-                    const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks + (size_t)kb * DP) + lane * 16;
+                    const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks) + (size_t)kb * RB + lane * 16;
                     const unsigned dst = ring + stage * Ge::STAGE;
-                    if (kb + 16 <= n) {  // the common case: the whole block is stored keys
+                    if (kb + 16 <= n32) {  // the common case: the whole block is stored keys
 #pragma unroll
                         for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512);
                     } else {
-                        const long long lim = n - kb - lane / CPR;
+                        const int lim = n32 - kb - lane / CPR;
 #pragma unroll
                         for (int k = 0; k < CPR / 2; ++k)
-                            cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, (long long)(k * RPI) < lim);
+                            cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, k * RPI < lim);
                     }
                 }
                 cpa_commit();
@@ -475,15 +484,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             int t = __shfl_sync(0xffffffffu, ca, 0), st = 0;
             bool pend = false;
             unsigned pb[4] = {0u, 0u, 0u, 0u};  // B fragments of the pending task's P (hi b0 b1, lo b0 b1)
-            k_issue(t, 0);
+            int k0 = t < ntask ? key0(t) : 0;  // first key of task t
+            k_issue(t, k0, 0);
             cpa_commit();  // stands for V(t-1)
             while (t < ntask) {
                 const int s1 = st == 2 ? 0 : st + 1;
                 const int s2 = st == 0 ? 2 : st - 1;  // stage of V(t-1)
-                const long long k0 = key0(t);
                 const int tn = __shfl_sync(0xffffffffu, cb, 0);
                 if (lane == 0 && tn < ntask) cb = atomicAdd(iscr + 3, 1);
-                k_issue(tn, s1);
+                const int kn = tn < ntask ? key0(tn) : 0;
+                k_issue(tn, kn, s1);
                 cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
                 __syncwarp();
                 // -- scores: 16 keys x [q0|q1|q2] per head
@@ -492,14 +502,17 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     float acc[NT][4];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
+                    const uint4* fq = reinterpret_cast<const uint4*>(fre);
 #pragma unroll
-                    for (int ks = 0; ks < KS; ++ks) {
-                        unsigned a[4];
-                        ldsm4(a, sb + a_off + (((2 * ks + a_hi) ^ (a_row & 7)) << 4));
+                    for (int k2 = 0; k2 < KS / 2; ++k2) {
+                        unsigned a0[4], a1[4];
+                        ldsm4(a0, sb + a_off + swz_off(2 * k2, a_hi, a_row));
+                        ldsm4(a1, sb + a_off + swz_off(2 * k2 + 1, a_hi, a_row));
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
-                            const uint2 b = fre[(ks * NT + nt) * 32 + lane];
-                            mma16816(acc[nt], a, b.x, b.y);
+                            const uint4 b = fq[(k2 * NT + nt) * 32 + lane];
+                            mma16816(acc[nt], a0, b.x, b.y);
+                            mma16816(acc[nt], a1, b.z, b.w);
                         }
                     }
 #pragma unroll
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const int pi = lane + 32 * j, rw = pi / G;
                     const float* c = ct + (rw < 16 ? rw : 15) * CT;
                     const float sc = (c[g_me] + c[G + g_me]) + c[2 * G + g_me];
-                    const bool valid = (G > 1 || lane < 16) && k0 + rw < n;
+                    const bool valid = (G > 1 || lane < 16) && k0 + rw < n32;
                     const bool sel = valid && (DENSE || sc >= tau_me + marg_me);
                     const bool u = !DENSE && valid && !sel && sc >= tau_me - marg_me;
                     s[j] = sc;
@@ -550,21 +563,21 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) {
                     const int pi = lane + 32 * j, rw = pi / G;
-                    const long long kk = k0 + rw;
-                    const bool valid = (G > 1 || lane < 16) && kk < n;
+                    const int kk = k0 + rw;
+                    const bool valid = (G > 1 || lane < 16) && kk < n32;
                     const bool sel = (selb >> j) & 1;
                     if (sel) {
                         ++my_sel;
                         if (!DENSE && p.bits)
                             atomicOr(p.bits + ((size_t)slot * G + g_me) * p.bits_words + (kk >> 5), 1u << (kk & 31));
                     }
-                    const bool att = sel || (valid && !p.strict && kk >= indexed);
+                    const bool att = sel || (valid && !p.strict && kk >= idx32);
                     my_att += att;
                     s[j] = att ? scale * s[j] : -INFINITY;
                     mloc = fmaxf(mloc, s[j]);
                     amask |= row_bits<G>(__ballot_sync(0xffffffffu, att)) << (j * (32 / G));
                 }
-                if (p.totals && lane == 0) t_keys += (k0 + 16 <= n) ? 16 : (n > k0 ? n - k0 : 0);
+                if (p.totals && lane == 0) t_keys += (k0 + 16 <= n32) ? 16 : (n32 > k0 ? n32 - k0 : 0);
                 float alpha = 1.0f;
                 unsigned nbf[4] = {0u, 0u, 0u, 0u};
                 if (amask) {
@@ -572,15 +585,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int of = 16; of >= G; of >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, of));
                     // lazy rescale: the reference max moves only when a score exceeds it by
-                    // more than 8 (weights stay <= e^8); o and l are rescaled only then
-                    if (mloc > mrun + 8.0f) {
-                        alpha = mrun == -INFINITY ? 0.0f : __expf(mrun - mloc);
+                    // more than 8 nats (weights stay <= e^8); o and l are rescaled only then.
+                    // The first move (from -inf) needs no rescale: o and l are still zero.
+                    if (mloc > mrun + 11.541560327111707f) {
+                        if (mrun != -INFINITY) alpha = ex2f(mrun - mloc);
                         mrun = mloc;
                     }
                     float lp = lpart * alpha;
 #pragma unroll
                     for (int j = 0; j < PPL; ++j) {
-                        const float pv = s[j] == -INFINITY ? 0.0f : __expf(s[j] - mrun);
+                        const float pv = s[j] == -INFINITY ? 0.0f : ex2f(s[j] - mrun);
                         lp += pv;
                         if (G > 1 || lane < 16) pbuf[lane + 32 * j] = pv;
                     }
@@ -614,21 +628,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 __syncwarp();  // K(t) and pbuf reads done
                 // -- V(t): attended rows into K(t)'s stage (same row positions)
-                if (amask) {  // RPI rows per warp instruction
-                    unsigned mm = amask;
+                if (amask) {  // RPI rows per warp instruction, from a rank list of the attended rows
+                    unsigned char* rows8 = reinterpret_cast<unsigned char*>(ct);  // the C tile is dead here
+                    if (lane < 16 && ((amask >> lane) & 1u)) rows8[__popc(amask & ((1u << lane) - 1u))] = (unsigned char)lane;
+                    __syncwarp();
+                    const int nr = __popc(amask), cc = lane % CPR;
                     const unsigned dst = ring + st * Ge::STAGE;
-                    const int cc = lane % CPR;
-                    const unsigned char* vsrc = reinterpret_cast<const unsigned char*>(Vs + (size_t)k0 * DP) + (lane % CPR) * 16;
-                    const int sub = lane / CPR;
-                    while (mm) {
-                        int rsel = -1;
-#pragma unroll
-                        for (int k = 0; k < RPI; ++k) {
-                            const int rr = mm ? __ffs(mm) - 1 : -1;
-                            mm &= mm - 1;
-                            if (k == sub) rsel = rr;
-                        }
-                        if (rsel >= 0) cpa16(dst + rsel * RB + ((cc ^ (rsel & 7)) << 4), vsrc + rsel * RB);
+                    const unsigned char* vsrc = reinterpret_cast<const unsigned char*>(Vs + (size_t)k0 * DP) + cc * 16;
+                    for (int k = lane / CPR; k < nr; k += RPI) {
+                        const int rsel = rows8[k];
+                        cpa16(dst + rsel * RB + ((cc ^ (rsel & 7)) << 4), vsrc + rsel * RB);
                     }
                 }
                 cpa_commit();
@@ -640,7 +649,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         unsigned a[4];
-                        ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
+                        ldsm4t(a, vb + swz_off(mt, v_hi, v_row));
                         mma16816(o[mt], a, pb[0], pb[1]);
                         if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                     }
@@ -661,6 +670,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 for (int e = 0; e < 4; ++e) pb[e] = nbf[e];
                 st = s1;
                 t = tn;
+                k0 = kn;
             }
             cpa_wait<0>();
             __syncwarp();
@@ -670,7 +680,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     unsigned a[4];
-                    ldsm4t(a, vb + (((2 * mt + v_hi) ^ (v_row & 7)) << 4));
+                    ldsm4t(a, vb + swz_off(mt, v_hi, v_row));
                     mma16816(o[mt], a, pb[0], pb[1]);
                     if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                 }
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         {
             float* w = wred + warp * Wd;
             if (lane < G) {
-                w[lane * (DP + 2)] = mrun;
+                w[lane * (DP + 2)] = mrun * 0.6931471805599453f;  // back to nats
                 w[lane * (DP + 2) + 1] = lpart;
             }
 #pragma unroll

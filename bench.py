@@ -17,9 +17,11 @@ N>1 (torchrun): the KV cache is sequence-sharded, 131072 keys per GPU per layer
 fused kernel on its shard and emits (m, l, o) partials, which are all-gathered
 over NCCL and merged with a log-sum-exp combine kernel.
 
---impl reference: the reference algorithm's CPU path (oracle/, a restatement
-of LouverCache::query with the reference defaults S=4, r=4, PCA tree, ball,
-FilterAlgo::Ta) on the same data, all host threads, rank 0 only.
+--impl reference: the reference library's own CPU path — its unmodified sources
+compiled here into oracle/_ref (the build travels with the repo) or, where that
+build is absent, the oracle restatement — LouverCache::query with the reference
+defaults S=4, r=4, PCA tree, ball, FilterAlgo::Ta, on the same data, all host
+threads, rank 0 only.
 """
 from __future__ import annotations
 
@@ -78,18 +80,61 @@ def gen_layer(cfg, layer, rank, threads):
     return K, V, Q
 
 
-def taus_device(torch, K, Q, G, frac):
-    """tau[b][hq] = ceil(frac*n)-th largest q.k (fp32 K as stored, fp64 scores)."""
+def top_scores(torch, K, Q, G, k):
+    """[B][H*G][k] descending: the k largest q.k per q head (bf16-rounded K as stored, fp64)."""
     B, H, n, d = K.shape
-    tau = np.zeros((B, H * G), np.float32)
-    k = max(1, int(math.ceil(frac * n)))
+    k = min(k, n)
+    out = torch.empty((B, H * G, k), dtype=torch.float64, device="cuda")
     for b in range(B):
         for h in range(H):
             kh = torch.from_numpy(K[b, h]).cuda().to(torch.bfloat16).double()
             qh = torch.from_numpy(Q[b, h * G:(h + 1) * G]).cuda().double()
             s = kh @ qh.T  # [n][G]
-            tau[b, h * G:(h + 1) * G] = torch.topk(s, k, dim=0).values[-1].float().cpu().numpy()
-    return tau
+            out[b, h * G:(h + 1) * G] = torch.topk(s, k, dim=0).values.T
+    return out
+
+
+def taus_device(torch, K, Q, G, frac, world=1, dist=None):
+    """tau[b][hq] = the ceil(frac * n_total)-th largest q.k over the whole (possibly
+    sequence-sharded) context: each rank's top-k candidates are all-gathered and the k-th
+    of their union is taken, so every rank uses the global threshold."""
+    n_total = K.shape[2] * world
+    k = max(1, int(math.ceil(frac * n_total)))
+    top = top_scores(torch, K, Q, G, k)
+    if world > 1:
+        pad = torch.full((top.shape[0], top.shape[1], k), -float("inf"), dtype=torch.float64, device="cuda")
+        pad[..., :top.shape[2]] = top
+        allt = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(allt, pad)
+        top = torch.topk(torch.cat(allt, dim=2), k, dim=2).values
+    return top[..., k - 1].float().cpu().numpy()
+
+
+def graph_time(torch, fn, reps, per):
+    """Median over `reps` replays of a CUDA graph of fn() (after warm-up), divided by `per`."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3 / per)
+    del g
+    return statistics.median(ts)
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -150,11 +195,20 @@ class ClockSampler:
 # --------------------------------------------------------------------- CPU baseline
 
 
-def oracle_cache_for(K_head, V_head):
+def cpu_reference():
+    """The reference library's CPU path: oracle/_ref (the reference's own sources compiled
+    here, travels with the repo; kind "reference") when present, else the oracle restatement
+    (kind "port")."""
     from oracle import pyoracle
 
-    return pyoracle.Cache(K_head.shape[1], pyoracle.cfg(4, 4, "pca_tree", "ball"), 128, keys=K_head,
-                          values=V_head)
+    ref = pyoracle.reference_module()
+    return (ref, "reference") if ref is not None else (pyoracle, "port")
+
+
+def oracle_cache_for(K_head, V_head, mod=None):
+    if mod is None:
+        mod = cpu_reference()[0]
+    return mod.Cache(K_head.shape[1], mod.cfg(4, 4, "pca_tree", "ball"), 128, keys=K_head, values=V_head)
 
 
 def cpu_baseline_sample(K, V, Q, tau, G, budget_s=20.0):
@@ -165,8 +219,9 @@ def cpu_baseline_sample(K, V, Q, tau, G, budget_s=20.0):
 
     Kh = torch.from_numpy(K[0, 0]).to(torch.bfloat16).float().numpy()
     Vh = torch.from_numpy(V[0, 0]).to(torch.bfloat16).float().numpy()
+    mod, kind = cpu_reference()
     t0 = time.perf_counter()
-    cache = oracle_cache_for(Kh, Vh)
+    cache = oracle_cache_for(Kh, Vh, mod)
     build_s = time.perf_counter() - t0
     times = []
     t_end = time.perf_counter() + budget_s
@@ -183,8 +238,9 @@ def cpu_baseline_sample(K, V, Q, tau, G, budget_s=20.0):
         "value": per_head * H_q * 1e6,
         "unit": UNIT,
         "cores": 1,
-        "kind": "port",
-        "sample": f"oracle LouverCache::query (S=4,r=4,pca_tree,ball,Ta) on kv head 0 of layer 0 "
+        "kind": kind,
+        "sample": f"{'reference build (oracle/_ref)' if kind == 'reference' else 'oracle port'} "
+                  f"LouverCache::query (S=4,r=4,pca_tree,ball,Ta) on kv head 0 of layer 0 "
                   f"({Kh.shape[0]} keys): median of {len(times)} single-thread q-head queries x {H_q} q heads; "
                   f"index build {build_s:.1f}s excluded",
     }
@@ -213,8 +269,9 @@ def run_reference(args, cfg):
                 for b in range(B) for hq in range(H * G)}
         for (b, hq), f in jobs.items():
             tau[b, hq] = f.result()
+        mod, kind = cpu_reference()
         t0 = time.perf_counter()
-        caches = {(b, h): ex.submit(oracle_cache_for, K[b, h], V[b, h]) for b in range(B) for h in range(H)}
+        caches = {(b, h): ex.submit(oracle_cache_for, K[b, h], V[b, h], mod) for b in range(B) for h in range(H)}
         caches = {k: f.result() for k, f in caches.items()}
     build_s = time.perf_counter() - t0
     heads = [(b, hq) for b in range(B) for hq in range(H * G)]
@@ -242,7 +299,7 @@ def run_reference(args, cfg):
         "config": {"workload": cfg["workload"] + " (one layer)", "n": n, "H_q": H * G, "H_kv": H, "d": d,
                    "batch": B, "selectivity": SELECTIVITY, "tau": "fixed, ceil(0.05 n)-th largest score",
                    "build": "reference defaults S=4 r=4 pca_tree ball, FilterAlgo::Ta"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"each step: {per_step} of {len(heads)} q-head queries in parallel on "
                                    f"{threads} threads, scaled to all q heads; index build {build_s:.1f}s excluded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -263,6 +320,7 @@ def main():
     ap.add_argument("--impl", default="louver", choices=["louver", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-dense-lib", action="store_true", help="skip the library (torch SDPA) dense decode")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -293,23 +351,18 @@ def main():
     e = 2 if cfg["dtype"] == "bf16" else 4
     build_cfg = BuildConfig(S=1, r=CELL, grouping="contiguous", enclosing="aabb")
 
-    layers, qs, taus, outs = [], [], [], []
+    layers, qs, taus, outs, kts, vts = [], [], [], [], [], []
     first = None
     t0 = time.perf_counter()
     for l in range(L):
         K, V, Q = gen_layer(cfg, l, rank, threads)
         layer = LouverLayer(d, H, G, B, n, build_cfg, buffer_capacity=128, dtype=cfg["dtype"])
         layer.build(K, V)
-        if world > 1:
-            # tau of the full (sharded) context: gather each rank's top-k candidates
-            tau_local = taus_device(torch, K, Q, G, SELECTIVITY)  # shard-local quantile
-            t = torch.from_numpy(tau_local).cuda()
-            allt = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(allt, t)
-            tau = torch.stack(allt).max(0).values.cpu().numpy()  # conservative: >= global k-th
-        else:
-            tau = taus_device(torch, K, Q, G, SELECTIVITY)
+        tau = taus_device(torch, K, Q, G, SELECTIVITY, world, dist if world > 1 else None)
         layers.append(layer)
+        if not args.no_dense_lib:  # bf16 [B][H][n][d] copies for the library dense decode (torch SDPA)
+            kts.append(torch.from_numpy(K).to("cuda", torch.bfloat16))
+            vts.append(torch.from_numpy(V).to("cuda", torch.bfloat16))
         qs.append(torch.from_numpy(Q).cuda())
         taus.append(torch.from_numpy(tau).cuda())
         outs.append(torch.zeros((B, H_q, d), dtype=torch.float32, device="cuda"))
@@ -408,16 +461,13 @@ def main():
     single_us = statistics.mean(kern_ms) * 1e3
     kern_us = us_layer if (graph is not None and world == 1) else single_us
 
-    # ---- dense full-scan baseline on the same layers
-    dense_ms = []
-    for i in range(reps):
-        l = i % L
-        ka.record()
-        layers[l].dense_decode(qs[l], outs[l])
-        kb.record()
-        kb.synchronize()
-        dense_ms.append(ka.elapsed_time(kb))
-    dense_us = statistics.mean(dense_ms) * 1e3
+    # ---- dense full-scan baselines on the same L layers, timed like the metric: a CUDA graph
+    # of L launches, median replay time / L after warm-up
+    def dense_all():
+        for l in range(L):
+            layers[l].dense_decode(qs[l], outs[l])
+
+    dense_us = graph_time(torch, dense_all, 50, L)
 
     # ---- the threshold oracle on the device: estimate_tau for every
     # q head of a layer from a 256-id reservoir per kv slot (budget:0.05), one launch
@@ -463,28 +513,23 @@ def main():
     except Exception as ex:  # pragma: no cover
         log(f"threshold oracle timing unavailable: {ex}")
 
-    # ---- library dense decode for reference: torch SDPA (flash / efficient kernel) on layer 0
+    # ---- library dense decode: torch SDPA (its flash / cuDNN kernel; the fastest dense decode
+    # in this image at C2, tools/dense_compare.py) over the same L layers, timed the same way
     sdpa_us = None
-    try:
-        import torch.nn.functional as F
-        K0, V0 = first[0], first[1]
-        kt = torch.from_numpy(K0).to("cuda", torch.bfloat16)
-        vt = torch.from_numpy(V0).to("cuda", torch.bfloat16)
-        qt = qs[0].to(torch.bfloat16).view(B, H_q, 1, d)
-        for _ in range(3):
-            F.scaled_dot_product_attention(qt, kt, vt, enable_gqa=True)
-        torch.cuda.synchronize()
-        sd = []
-        for _ in range(reps):
-            ka.record()
-            F.scaled_dot_product_attention(qt, kt, vt, enable_gqa=True)
-            kb.record()
-            kb.synchronize()
-            sd.append(ka.elapsed_time(kb))
-        sdpa_us = statistics.mean(sd) * 1e3
-        del kt, vt
-    except Exception as ex:  # pragma: no cover - library path unavailable
-        log(f"sdpa baseline unavailable: {ex}")
+    if kts:
+        try:
+            import torch.nn.functional as F
+
+            qb = [q.to(torch.bfloat16).view(B, H_q, 1, d) for q in qs]
+
+            def sdpa_all():
+                for l in range(L):
+                    F.scaled_dot_product_attention(qb[l], kts[l], vts[l], enable_gqa=True)
+
+            sdpa_us = graph_time(torch, sdpa_all, 50, L)
+        except Exception as ex:  # pragma: no cover - library path unavailable
+            log(f"sdpa baseline unavailable: {ex}")
+        del kts[:], vts[:]
 
     # ---- end to end through the public API with host buffers (pinned), one decode step at a
     # time: the step's q and tau go host->device in one copy each, the L layer queries run
@@ -607,8 +652,11 @@ def main():
         "dense": {"us_per_layer": dense_us, "bytes": dense_bytes,
                   "achieved_gbs": dense_bytes / (dense_us * 1e-6) / 1e9,
                   "speedup_vs_dense": dense_us / kern_us,
+                  "how": "CUDA graph of L layer launches, median of 50 replays / L (same as the metric)",
                   "torch_sdpa_us_per_layer": sdpa_us,
-                  "speedup_vs_torch_sdpa": (sdpa_us / kern_us) if sdpa_us else None},
+                  "speedup_vs_torch_sdpa": (sdpa_us / kern_us) if sdpa_us else None,
+                  "best_dense_us_per_layer": min(x for x in (dense_us, sdpa_us) if x),
+                  "speedup_vs_best_dense": min(x for x in (dense_us, sdpa_us) if x) / kern_us},
         "e2e": {"value": e2e_us, "unit": UNIT, "h2d_bytes_per_step": L * rows * (d + 1) * 4,
                 "d2h_bytes_per_step": L * rows * d * 4,
                 "how": ("host wall clock per decode step / L: pinned q, tau -> device (one copy each), L x "

@@ -121,6 +121,32 @@ def main():
     except Exception as e:  # pragma: no cover
         res["flashinfer_single_decode"] = {"error": str(e)[:300]}
 
+    try:  # TensorRT-LLM-gen decode kernels shipped as sm_100 cubins (flashinfer-cubin), paged HND
+        import flashinfer
+
+        page = 128
+        npg = n // page
+        # [pages][H][page][d] strided views of the [B=1][H][n][d] caches (no copy)
+        kp = [k[0].view(H, npg, page, d).permute(1, 0, 2, 3) for k in kts]
+        vp = [v[0].view(H, npg, page, d).permute(1, 0, 2, 3) for v in vts]
+        qt = [q.to(torch.bfloat16)[0] for q in qs]  # [Hq][d]
+        ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+        bt = torch.arange(npg, dtype=torch.int32, device="cuda").view(1, npg)
+        sl = torch.tensor([n], dtype=torch.int32, device="cuda")
+        to = [torch.empty((Hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+
+        def trt():
+            for l in range(L):
+                flashinfer.decode.trtllm_batch_decode_with_kv_cache(
+                    qt[l], (kp[l], vp[l]), ws, bt, sl, n, bmm1_scale=1.0 / math.sqrt(d), bmm2_scale=1.0,
+                    out=to[l], kv_layout="HND")
+
+        trt()
+        torch.cuda.synchronize()
+        res["flashinfer_trtllm_gen_decode"] = {"us": graph_time(trt), "max_rel_err": err(to[0].float())}
+    except Exception as e:  # pragma: no cover
+        res["flashinfer_trtllm_gen_decode"] = {"error": str(e)[:300]}
+
     try:
         from flash_attn import flash_attn_with_kvcache
 

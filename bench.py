@@ -360,9 +360,10 @@ def main():
         layer.build(K, V)
         tau = taus_device(torch, K, Q, G, SELECTIVITY, world, dist if world > 1 else None)
         layers.append(layer)
-        if not args.no_dense_lib:  # bf16 [B][H][n][d] copies for the library dense decode (torch SDPA)
-            kts.append(torch.from_numpy(K).to("cuda", torch.bfloat16))
-            vts.append(torch.from_numpy(V).to("cuda", torch.bfloat16))
+        if not args.no_dense_lib:  # [B][H][n][d] copies (config dtype) for the library dense decode (SDPA)
+            tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+            kts.append(torch.from_numpy(K).to("cuda", tdt))
+            vts.append(torch.from_numpy(V).to("cuda", tdt))
         qs.append(torch.from_numpy(Q).cuda())
         taus.append(torch.from_numpy(tau).cuda())
         outs.append(torch.zeros((B, H_q, d), dtype=torch.float32, device="cuda"))
@@ -520,7 +521,7 @@ def main():
         try:
             import torch.nn.functional as F
 
-            qb = [q.to(torch.bfloat16).view(B, H_q, 1, d) for q in qs]
+            qb = [q.to(kts[0].dtype).view(B, H_q, 1, d) for q in qs]
 
             def sdpa_all():
                 for l in range(L):

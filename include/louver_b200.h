@@ -172,7 +172,9 @@ int lv_read_rows(const lv_ctx* ctx, int slot, int64_t first, int64_t count, int 
 
 /* query.cpp:11-20 on the device: bitmap of ids j < limit with dot(q, k_j) >= tau
  * for every q head (normative dot, bit-exact). q, tau as in lv_query (`where`
- * applies to them); sel_bits is DEVICE [batch][H_q][lv_bitmap_words()]. */
+ * applies to them); sel_bits is DEVICE [batch][H_q][lv_bitmap_words()].
+ * limit == -1: every key stored when the kernel runs (the device counter; for
+ * CUDA-graph replay, where a host-side limit would be frozen at capture). */
 int lv_brute_force_range(lv_ctx* ctx, const float* q, const float* tau, int64_t limit, int where,
                          uint32_t* sel_bits, void* stream);
 
@@ -238,6 +240,32 @@ int lv_estimate_tau(lv_ctx* ctx, const uint32_t* ids, int64_t count, int64_t ld,
  * e.g. lv_query's sel_bits against lv_brute_force_range's. Enqueue-only. */
 int lv_bits_diff(const uint32_t* a, const uint32_t* b, int64_t words, int64_t rows, int32_t* violations,
                  void* stream);
+
+/* Decode-loop plumbing for CUDA-graph replay of run_decode_sim (bench.cpp:54-136):
+ * a DEVICE int64 step counter t selects each step's slice, so one captured decode
+ * step (inputs in, estimate_tau, lv_query, lv_push_key, statistics out) replays the
+ * whole loop with no host work. All pointers DEVICE; enqueue-only; capturable.
+ * bytes and strides are multiples of 4.
+ *   lv_step_load:      dst[0, bytes) <- src[t * stride, t * stride + bytes)
+ *   lv_step_store:     dst[t * stride, + bytes) <- src[0, bytes)
+ *   lv_step_reservoir: s = slot_of_step[t]; if s >= 0: ids[j * ld + s] = row0 + t for each of
+ *                      the nslots reservoir copies — the write of Reservoir::update
+ *                      (threshold.cpp:40-55), drawn on the host in advance
+ *   lv_step_advance:   t += 1 */
+/* Several step-indexed copies in one launch (up to 8): dir 0 = load, 1 = store. */
+typedef struct lv_step_copy {
+    const void* src;
+    void* dst;
+    int64_t stride;
+    int64_t bytes;
+    int dir;
+} lv_step_copy;
+int lv_step_copies(const int64_t* step, const lv_step_copy* copies, int ncopies, void* stream);
+int lv_step_load(const int64_t* step, const void* src, int64_t stride, void* dst, int64_t bytes, void* stream);
+int lv_step_store(const int64_t* step, const void* src, void* dst, int64_t stride, int64_t bytes, void* stream);
+int lv_step_reservoir(const int64_t* step, const int32_t* slot_of_step, int64_t row0, uint32_t* ids, int nslots,
+                      int64_t ld, void* stream);
+int lv_step_advance(int64_t* step, void* stream);
 
 /* --- Snapshots (io.hpp:40-51, io.cpp:205-317) --------------------------------
  * "LVKD" dataset: magic, version 1, n, d (u32 LE), n*d f32 row-major. With

@@ -16,7 +16,8 @@ from .threshold import (  # noqa: F401
     parse_oracle,
 )
 from .snapshot import load_dataset, load_index, save_dataset, save_index  # noqa: F401
-from .decode_sim import DecodeSimConfig, MetricsReport, ThresholdSource, run_decode_sim  # noqa: F401
+from .decode_sim import (DecodeSimConfig, GraphDecodeReport, MetricsReport, ThresholdSource,  # noqa: F401
+                         run_decode_graph, run_decode_sim)
 from .louver import (  # noqa: F401
     AttentionResult,
     BuildConfig,
@@ -36,6 +37,6 @@ __all__ = [
     "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
-    "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim",
+    "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim", "GraphDecodeReport", "run_decode_graph",
     "save_dataset", "load_dataset", "save_index", "load_index",
 ]

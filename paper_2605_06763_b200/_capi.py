@@ -68,6 +68,11 @@ def _load(path: str) -> C.CDLL:
     return C.CDLL(path)
 
 
+class lv_step_copy(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("stride", C.c_int64), ("bytes", C.c_int64),
+                ("dir", C.c_int)]
+
+
 _lib = None
 _synth = None
 
@@ -114,6 +119,11 @@ _SIGS = {
     "lv_save_index": (C.c_int, [_P, C.c_int, C.c_char_p]),
     "lv_load_index": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_int64), _P]),
     "lv_bits_diff": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P]),
+    "lv_step_copies": (C.c_int, [_P, _P, C.c_int, _P]),
+    "lv_step_load": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
+    "lv_step_store": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
+    "lv_step_reservoir": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int, C.c_int64, _P]),
+    "lv_step_advance": (C.c_int, [_P, _P]),
     "lv_estimate_tau": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P]),
 }
 

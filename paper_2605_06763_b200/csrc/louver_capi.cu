@@ -743,7 +743,8 @@ int lv_dense_decode(lv_ctx* c, const float* q, float scale, int where, float* ou
 int lv_brute_force_range(lv_ctx* c, const float* q, const float* tau, int64_t limit, int where,
                          uint32_t* sel_bits, void* stream) {
     if (!c || !q || !tau || !sel_bits) return fail(LV_EINVAL, "lv_brute_force_range: null argument");
-    if (limit < 0 || limit > c->n) return fail(LV_EINVAL, "brute_force_range: limit > n");
+    if (limit < -1 || limit > c->n) return fail(LV_EINVAL, "brute_force_range: limit > n");
+    if (limit == -1) limit = c->cap;  // every stored key: the kernel clamps to the DEVICE count
     cudaStream_t st = S(stream);
     Workspace w;
     carve(c, reinterpret_cast<unsigned char*>(c->ws_mem), &w);
@@ -904,6 +905,64 @@ int lv_bits_diff(const uint32_t* a, const uint32_t* b, int64_t words, int64_t ro
     if (!a || !b || !violations || words < 0 || rows < 0) return fail(LV_EINVAL, "lv_bits_diff: bad arguments");
     if (rows == 0 || words == 0) return LV_OK;
     lvkt::bits_diff_kernel<<<(unsigned)rows, 256, 0, S(stream)>>>(a, b, words, violations);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_step_load(const int64_t* step, const void* src, int64_t stride, void* dst, int64_t bytes, void* stream) {
+    if (!step || !src || !dst || stride < 0 || bytes < 0 || bytes % 4 || stride % 4)
+        return fail(LV_EINVAL, "lv_step_load: bad arguments (4-byte multiples required)");
+    if (bytes == 0) return LV_OK;
+    const long long w = bytes / 4;
+    lvkt::step_copy_kernel<<<(unsigned)std::min<long long>((w + 255) / 256, 148), 256, 0, S(stream)>>>(
+        reinterpret_cast<const long long*>(step), (const uint32_t*)src, (uint32_t*)dst, stride / 4, w, 0);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_step_store(const int64_t* step, const void* src, void* dst, int64_t stride, int64_t bytes, void* stream) {
+    if (!step || !src || !dst || stride < 0 || bytes < 0 || bytes % 4 || stride % 4)
+        return fail(LV_EINVAL, "lv_step_store: bad arguments (4-byte multiples required)");
+    if (bytes == 0) return LV_OK;
+    const long long w = bytes / 4;
+    lvkt::step_copy_kernel<<<(unsigned)std::min<long long>((w + 255) / 256, 148), 256, 0, S(stream)>>>(
+        reinterpret_cast<const long long*>(step), (const uint32_t*)src, (uint32_t*)dst, stride / 4, w, 1);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_step_copies(const int64_t* step, const lv_step_copy* copies, int ncopies, void* stream) {
+    if (!step || !copies || ncopies < 1 || ncopies > 8) return fail(LV_EINVAL, "lv_step_copies: 1..8 copies");
+    lvkt::StepCopies cs{};
+    long long maxw = 0;
+    for (int i = 0; i < ncopies; ++i) {
+        const lv_step_copy& c = copies[i];
+        if (!c.src || !c.dst || c.stride < 0 || c.bytes < 0 || c.bytes % 4 || c.stride % 4 || (c.dir != 0 && c.dir != 1))
+            return fail(LV_EINVAL, "lv_step_copies: bad copy (4-byte multiples, dir 0 or 1)");
+        cs.c[i] = {(const uint32_t*)c.src, (uint32_t*)c.dst, c.stride / 4, c.bytes / 4, c.dir};
+        maxw = std::max<long long>(maxw, c.bytes / 4);
+    }
+    cs.n = ncopies;
+    if (maxw == 0) return LV_OK;
+    dim3 grid((unsigned)std::min<long long>((maxw + 255) / 256, 64), (unsigned)ncopies);
+    lvkt::step_copies_kernel<<<grid, 256, 0, S(stream)>>>(reinterpret_cast<const long long*>(step), cs);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_step_reservoir(const int64_t* step, const int32_t* slot_of_step, int64_t row0, uint32_t* ids, int nslots,
+                      int64_t ld, void* stream) {
+    if (!step || !slot_of_step || !ids || row0 < 0 || nslots < 1 || nslots > 1024 || ld < 0)
+        return fail(LV_EINVAL, "lv_step_reservoir: bad arguments");
+    lvkt::step_reservoir_kernel<<<1, nslots, 0, S(stream)>>>(reinterpret_cast<const long long*>(step), slot_of_step,
+                                                            row0, ids, nslots, ld);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
+int lv_step_advance(int64_t* step, void* stream) {
+    if (!step) return fail(LV_EINVAL, "lv_step_advance: null step");
+    lvkt::step_advance_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<long long*>(step));
     LV_CUDA(cudaGetLastError());
     return LV_OK;
 }

@@ -170,4 +170,51 @@ __global__ void bits_diff_kernel(const uint32_t* __restrict__ a, const uint32_t*
     if (diff && threadIdx.x == 0) atomicAdd(violations, 1);
 }
 
+// ---- decode-loop plumbing for CUDA-graph replay (bench.cpp:71-120): a device step counter
+// selects each step's inputs, so one captured step replays the whole loop with no host work
+
+// dir 0: dst[0, words) <- src[t * stride ..];  dir 1: dst[t * stride ..] <- src[0, words)
+__global__ void step_copy_kernel(const long long* __restrict__ step, const uint32_t* __restrict__ src,
+                                 uint32_t* __restrict__ dst, long long stride_words, long long words, int dir) {
+    const long long off = *step * stride_words;
+    const uint32_t* s = dir == 0 ? src + off : src;
+    uint32_t* d = dir == 0 ? dst : dst + off;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (long long)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+struct StepCopy {
+    const uint32_t* src;
+    uint32_t* dst;
+    long long stride_words;
+    long long words;
+    int dir;  // 0: dst <- src[t * stride]; 1: dst[t * stride] <- src
+};
+struct StepCopies {
+    StepCopy c[8];
+    int n;
+};
+
+// every copy of a step in one launch (blockIdx.y = copy)
+__global__ void step_copies_kernel(const long long* __restrict__ step, const __grid_constant__ StepCopies cs) {
+    if ((int)blockIdx.y >= cs.n) return;
+    const StepCopy& c = cs.c[blockIdx.y];
+    const long long off = *step * c.stride_words;
+    const uint32_t* s = c.dir == 0 ? c.src + off : c.src;
+    uint32_t* d = c.dir == 0 ? c.dst : c.dst + off;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.words; i += (long long)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+// Reservoir::update's write (threshold.cpp:40-55), drawn on the host in advance: the step's
+// admitted slot (or -1) receives the step's arena row
+__global__ void step_reservoir_kernel(const long long* __restrict__ step, const int* __restrict__ slot_of_step,
+                                      long long row0, uint32_t* __restrict__ ids, int nslots, long long ld) {
+    const long long t = *step;
+    const int slot = slot_of_step[t];
+    if (slot >= 0 && (int)threadIdx.x < nslots) ids[threadIdx.x * ld + slot] = (uint32_t)(row0 + t);
+}
+
+__global__ void step_advance_kernel(long long* step) { *step += 1; }
+
 }  // namespace lvkt

@@ -240,4 +240,159 @@ def run_decode_sim(keys, values, queries, cfg: DecodeSimConfig, prefill: int = 0
     return rep
 
 
-__all__ = ["ThresholdSource", "DecodeSimConfig", "MetricsReport", "run_decode_sim", "speedup_estimate"]
+@dataclasses.dataclass
+class GraphDecodeReport:
+    """Statistics of ``run_decode_graph`` (per q head means over the decode steps)."""
+
+    steps: int = 0
+    flushes: int = 0
+    n_final: int = 0
+    violations: int = -1              # -1: not verified
+    us_per_step: float = 0.0          # device time of the replayed step graphs / steps
+    mean_selected: float = 0.0        # per q head per step
+    mean_attended: float = 0.0
+    mean_keys_scanned: float = 0.0
+    mean_f_scan: float = 0.0          # keys scanned / keys stored before the step
+    mean_tau: float = 0.0
+    selected: Optional[np.ndarray] = None  # [steps][rows] per step and q head
+    taus: Optional[np.ndarray] = None      # [steps][rows]
+
+
+def run_decode_graph(keys, values, queries, H_kv: int, G: int, cfg: DecodeSimConfig, prefill: int,
+                     batch: int = 1, dtype: str = "bf16", steps_per_graph: int = 16,
+                     verify: bool = False) -> GraphDecodeReport:
+    """The decode loop of bench.cpp:71-120 for a whole attention layer (``batch`` x ``H_kv``
+    kv slots, ``G`` q heads each), captured as CUDA graphs and replayed with no host work
+    per step. keys, values: [rows][batch * H_kv][d]; queries: [rows][batch * H_kv * G][d]
+    (float32, row t drives step t). Rows [0, prefill) are the prompt, indexed at once;
+    steps prefill .. rows - 1 each run, on the device:
+
+      load q_t, k_t, v_t (a device step counter selects the slice)
+      tau  = estimate_tau over the reservoir (oracle source) or the fixed tau
+      lv_query (selected / attended / scanned counts logged per step)
+      [verify: brute_force_range over every stored key, bitmap compare]
+      lv_push_key(k_t, v_t)  (flush at B inside the insert kernel)
+      the reservoir's write for row t (its draws are the reference's mt19937_64,
+      made on the host in advance: they depend only on capacity, seed and t)
+
+    With the oracle source the reservoir must be full after the prompt (prefill >=
+    capacity), so every step samples the same number of rows, as a captured launch
+    requires."""
+    import torch
+
+    keys = np.ascontiguousarray(keys, np.float32)
+    values = np.ascontiguousarray(values, np.float32)
+    queries = np.ascontiguousarray(queries, np.float32)
+    rows, slots, d = keys.shape
+    rq = queries.shape[1]
+    if slots != batch * H_kv or rq != slots * G or values.shape != keys.shape or queries.shape[0] != rows:
+        raise ValueError("run_decode_graph: shapes must be keys/values [rows][batch*H_kv][d], queries [rows][rows_q][d]")
+    if not 0 < prefill < rows:
+        raise ValueError("run_decode_graph: 0 < prefill < rows required")
+    oracle = cfg.threshold.oracle if cfg.threshold.fixed_tau is None else None
+    if oracle is None and cfg.threshold.fixed_tau is None:
+        raise ValueError("run_decode_graph: no threshold source")
+    if oracle is not None:
+        oracle.validate()
+        if prefill < cfg.reservoir_capacity:
+            raise ValueError("run_decode_graph: the reservoir must be full after the prompt")
+    steps = rows - prefill
+    spg = max(1, min(steps_per_graph, steps))
+    while steps % spg:
+        spg -= 1
+    dev = torch.device("cuda")
+    lib = _capi.lib()
+    layer = LouverLayer(d, H_kv, G, batch, rows, cfg.build, buffer_capacity=cfg.buffer_capacity, dtype=dtype)
+    layer.build(np.ascontiguousarray(keys[:prefill].reshape(prefill, batch, H_kv, d).transpose(1, 2, 0, 3)),
+                np.ascontiguousarray(values[:prefill].reshape(prefill, batch, H_kv, d).transpose(1, 2, 0, 3)))
+    # the reservoir's admissions for every row, drawn now (threshold.cpp:40-55)
+    res = Reservoir(cfg.reservoir_capacity, cfg.seed)
+    slot_of = np.full((rows,), -1, np.int32)
+    for t in range(rows):
+        slot_of[t] = res.update(t)
+    res0 = Reservoir(cfg.reservoir_capacity, cfg.seed)
+    for t in range(prefill):
+        res0.update(t)
+    cap = cfg.reservoir_capacity
+    ids_d = torch.from_numpy(np.tile(res0.ids().astype(np.int32)[None], (slots, 1))).to(dev)
+    slot_d = torch.from_numpy(slot_of).to(dev)
+    k_d, v_d, q_d = (torch.from_numpy(a).to(dev) for a in (keys, values, queries))
+    q_buf = torch.zeros((batch, H_kv * G, d), dtype=torch.float32, device=dev)
+    k_buf = torch.zeros((batch, H_kv, d), dtype=torch.float32, device=dev)
+    v_buf = torch.zeros_like(k_buf)
+    fill = float(cfg.threshold.fixed_tau) if oracle is None else 0.0
+    tau_buf = torch.full((batch, H_kv * G), fill, dtype=torch.float32, device=dev)
+    out_buf = torch.zeros((batch, H_kv * G, d), dtype=torch.float32, device=dev)
+    counts = torch.zeros((batch, H_kv * G, 4), dtype=torch.int32, device=dev)
+    cnt_log = torch.zeros((rows, rq, 4), dtype=torch.int32, device=dev)
+    tau_log = torch.zeros((rows, rq), dtype=torch.float32, device=dev)
+    step_d = torch.tensor([prefill], dtype=torch.int64, device=dev)
+    words = layer.bitmap_words
+    bits = torch.zeros((rq, words), dtype=torch.int32, device=dev) if verify else None
+    ref_bits = torch.zeros_like(bits) if verify else None
+    viol = torch.zeros((1,), dtype=torch.int32, device=dev)
+    ctx = layer._ctx
+
+    cp = _capi.lv_step_copy
+    loads = (cp * 3)(cp(q_d.data_ptr(), q_buf.data_ptr(), rq * d * 4, rq * d * 4, 0),
+                     cp(k_d.data_ptr(), k_buf.data_ptr(), slots * d * 4, slots * d * 4, 0),
+                     cp(v_d.data_ptr(), v_buf.data_ptr(), slots * d * 4, slots * d * 4, 0))
+    stores = (cp * 2)(cp(counts.data_ptr(), cnt_log.data_ptr(), rq * 16, rq * 16, 1),
+                      cp(tau_buf.data_ptr(), tau_log.data_ptr(), rq * 4, rq * 4, 1))
+
+    def one_step(st):
+        sp = step_d.data_ptr()
+        check(lib.lv_step_copies(sp, loads, 3, st), "lv_step_copies")
+        if oracle is not None:
+            estimate_tau_layer(layer, ids_d, cap, q_buf, oracle, tau_buf, stream=st)
+        counts.zero_()
+        if verify:
+            bits.zero_()
+        layer.query_device(q_buf, tau_buf, out_buf, strict=cfg.strict_threshold, counts=counts, sel_bits=bits,
+                           stream=st)
+        if verify:
+            check(lib.lv_brute_force_range(ctx.h, q_buf.data_ptr(), tau_buf.data_ptr(), -1, _capi.LV_DEVICE,
+                                           ref_bits.data_ptr(), st), "lv_brute_force_range")
+            check(lib.lv_bits_diff(bits.data_ptr(), ref_bits.data_ptr(), words, rq, viol.data_ptr(), st),
+                  "lv_bits_diff")
+        check(lib.lv_step_copies(sp, stores, 2, st), "lv_step_copies")
+        layer.push_key(k_buf, v_buf, stream=st)
+        check(lib.lv_step_reservoir(sp, slot_d.data_ptr(), 0, ids_d.data_ptr(), slots, cap, st), "lv_step_reservoir")
+        check(lib.lv_step_advance(sp, st), "lv_step_advance")
+
+    stream = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=stream):
+        st = torch.cuda.current_stream().cuda_stream
+        for _ in range(spg):
+            one_step(st)
+    layer.sync_counters()  # capture advanced the host mirrors; the device counters did not move
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(steps // spg):
+        graph.replay()
+    b.record()
+    torch.cuda.synchronize()
+    layer.sync_counters()
+    rep = GraphDecodeReport(steps=steps, flushes=layer.flush_count, n_final=layer.n,
+                            us_per_step=a.elapsed_time(b) * 1e3 / steps)
+    if verify:
+        rep.violations = int(viol.item())
+    cl = cnt_log[prefill:].cpu().numpy().astype(np.float64)
+    tl = tau_log[prefill:].cpu().numpy().astype(np.float64)
+    n_before = np.arange(prefill, rows, dtype=np.float64)[:, None]
+    rep.mean_selected = float(cl[..., 0].mean())
+    rep.mean_attended = float(cl[..., 1].mean())
+    rep.mean_keys_scanned = float(cl[..., 2].mean())
+    rep.mean_f_scan = float((cl[..., 2] / n_before).mean())
+    rep.mean_tau = float(tl.mean())
+    rep.selected = cl[..., 0].astype(np.int64)
+    rep.taus = tl.astype(np.float32)
+    del graph
+    return rep
+
+
+__all__ = ["ThresholdSource", "DecodeSimConfig", "MetricsReport", "run_decode_sim", "speedup_estimate",
+           "GraphDecodeReport", "run_decode_graph"]

@@ -111,3 +111,54 @@ def test_decode_matches_oracle_loop(torch, oracle, oc, strict):
     assert rep.mean_retrieved == pytest.approx(m_ret, rel=0, abs=1e-9)
     assert rep.mean_tau == pytest.approx(m_tau, rel=1e-12, abs=1e-12)
     assert rep.median_query_us > 0.0
+
+
+# ---------------------------------------------------------------------------------------------
+# run_decode_graph: the whole decode loop of a GQA layer captured as CUDA graphs (SURVEY §8(f)
+# row 2 at the C2 head shape). Checked step by step against the oracle: every step's τ is the
+# oracle's estimate_tau over the reservoir the reference would hold, and every step's selected
+# count is the oracle's brute_force_range over the keys stored before the step.
+
+
+def _graph_case(H_kv, G, d, prefill, steps, seed):
+    from paper_2605_06763_b200 import synth
+
+    rows = prefill + steps
+    K = np.stack([synth.keys(rows, d, seed + 7 * h) for h in range(H_kv)], axis=1)       # [rows][H][d]
+    V = np.stack([synth.keys(rows, d, seed + 7 * h + 1) for h in range(H_kv)], axis=1)
+    Q = np.stack([synth.queries(rows * G, d, seed + 7 * h).reshape(rows, G, d) for h in range(H_kv)],
+                 axis=1).reshape(rows, H_kv * G, d)
+    return K.astype(np.float32), V.astype(np.float32), Q.astype(np.float32)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_graph_decode_matches_oracle(torch, dtype):
+    from oracle import pyoracle
+    from paper_2605_06763_b200 import Reservoir
+    from paper_2605_06763_b200.decode_sim import run_decode_graph
+
+    H_kv, G, d, prefill, steps, B, cap = 2, 4, 128, 512, 192, 32, 64
+    K, V, Q = _graph_case(H_kv, G, d, prefill, steps, 5)
+    if dtype == "bf16":  # the oracle sees the stored (bf16) keys
+        K = torch.from_numpy(K).to(torch.bfloat16).float().numpy()
+        V = torch.from_numpy(V).to(torch.bfloat16).float().numpy()
+    cfg = DecodeSimConfig(build=BuildConfig(1, 16, "contiguous", "aabb", 0), buffer_capacity=B,
+                          threshold=ThresholdSource(oracle=OracleConfig(OracleVariant.Budget, 0, 0.05)),
+                          reservoir_capacity=cap, seed=3)
+    rep = run_decode_graph(K, V, Q, H_kv, G, cfg, prefill, dtype=dtype, steps_per_graph=8, verify=True)
+    assert rep.steps == steps and rep.n_final == prefill + steps
+    assert rep.flushes == steps // B  # the prompt is indexed at build, not flushed
+    assert rep.violations == 0
+    res = Reservoir(cap, 3)
+    for t in range(prefill):
+        res.update(t)
+    for i, t in enumerate(range(prefill, prefill + steps)):
+        ids = res.ids()
+        for hq in range(H_kv * G):
+            h = hq // G
+            want_tau = pyoracle.estimate_tau(K[ids, h], Q[t, hq], 4, alpha=0.05)
+            assert rep.taus[i, hq] == want_tau, (t, hq)
+            want = pyoracle.brute_force_range(K[:t, h], Q[t, hq], want_tau)
+            assert rep.selected[i, hq] == want.size, (t, hq)
+        res.update(t)

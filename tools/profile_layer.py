@@ -25,6 +25,17 @@ def main():
     layer.build(K, V)
     q, t = torch.from_numpy(Q).cuda(), torch.from_numpy(tau).cuda()
     out = torch.zeros((cfg["batch"], cfg["H_kv"] * G, cfg["d"]), device="cuda")
+    if which == "insert":  # one decode step's key per kv slot, a few steps
+        kk = torch.from_numpy(K[:, :, :reps].transpose(2, 0, 1, 3).copy()).cuda()  # [reps][B][H][d]
+        layer2 = LouverLayer(cfg["d"], cfg["H_kv"], G, cfg["batch"], cfg["n"] + 1024,
+                             BuildConfig(S=1, r=bench.CELL, grouping="contiguous", enclosing="aabb"),
+                             dtype=cfg["dtype"])
+        layer2.build(K, V)
+        for i in range(reps):
+            layer2.push_key(kk[i], kk[i])
+        torch.cuda.synchronize()
+        print("done insert")
+        return
     for _ in range(reps):
         if which in ("both", "query"):
             layer.query_device(q, t, out)

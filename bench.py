@@ -539,8 +539,11 @@ def main():
     q_all_h = torch.stack([q.cpu() for q in qs]).pin_memory()      # [L][B][H_q][d]
     t_all_h = torch.stack([t.cpu() for t in taus]).pin_memory()    # [L][B][H_q]
     o_all_h = torch.empty((L, B, H_q, d), dtype=torch.float32).pin_memory()
-    q_all_d, t_all_d = torch.empty_like(q_all_h, device="cuda"), torch.empty_like(t_all_h, device="cuda")
-    o_all_d = torch.empty((L, B, H_q, d), dtype=torch.float32, device="cuda")
+
+    from paper_2605_06763_b200 import query_layers_host
+
+    q_np, t_np, o_np = q_all_h.numpy(), t_all_h.numpy(), o_all_h.numpy()
+    cur = torch.cuda.current_stream().cuda_stream
 
     def e2e_step():
         if world > 1:  # the sharded step: per-layer inputs, shard queries + all-gather + LSE merge
@@ -550,13 +553,9 @@ def main():
             step()
             for l in range(L):
                 o_all_h[l].copy_(outs[l], non_blocking=True)
-        else:
-            q_all_d.copy_(q_all_h, non_blocking=True)
-            t_all_d.copy_(t_all_h, non_blocking=True)
-            for l in range(L):
-                layers[l].query_device(q_all_d[l], t_all_d[l], o_all_d[l])
-            o_all_h.copy_(o_all_d, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+            torch.cuda.current_stream().synchronize()
+        else:  # the C ABI's host-buffer decode step (lv_query_layers): one copy in, L queries, one out
+            query_layers_host(layers, q_np, t_np, o_np, stream=cur)
 
     e2e_steps = max(5, min(50, args.steps))
     for _ in range(3):
@@ -660,8 +659,12 @@ def main():
                   "speedup_vs_best_dense": min(x for x in (dense_us, sdpa_us) if x) / kern_us},
         "e2e": {"value": e2e_us, "unit": UNIT, "h2d_bytes_per_step": L * rows * (d + 1) * 4,
                 "d2h_bytes_per_step": L * rows * d * 4,
-                "how": ("host wall clock per decode step / L: pinned q, tau -> device (one copy each), L x "
-                        "lv_query on the stream, L outputs -> pinned host (one copy), stream sync"),
+                "how": ("host wall clock per decode step / L through the C ABI with HOST buffers: "
+                        "lv_query_layers(pinned q, tau, out): one host->device copy of every layer's q and tau, "
+                        "L fused layer queries, one device->host copy of the outputs, one stream sync"
+                        if world == 1 else
+                        "host wall clock per sharded decode step / L: pinned q, tau -> device, L x (lv_query partial, "
+                        "NCCL all-gather, lv_lse_merge), outputs -> pinned host, stream sync"),
                 "per_layer_sync_us": e2e_sync_us,
                 "per_layer_sync_how": "one synchronous lv_query(LV_HOST) per layer: pinned q/tau H2D, kernel, pinned out D2H, sync"},
         "clocks": clocks.summary(),

@@ -106,6 +106,9 @@ typedef struct {
                            group), keys loaded (union), values loaded (union) — summed over slots */
     void* workspace;    /* optional DEVICE scratch of lv_query_workspace_bytes() bytes */
     void* stream;       /* cudaStream_t */
+    uint32_t* cand_bits; /* optional DEVICE [batch][H_kv][lv_bitmap_words()]: the candidate set of
+                            query_ta / query_full_subspace (query.hpp:48-58) — every INDEXED key
+                            of a cell whose bound reaches any q head's threshold (fp32 caches) */
 } lv_query_args;
 
 const char* lv_last_error(void);
@@ -140,6 +143,18 @@ int lv_flush(lv_ctx* ctx, void* stream);
 
 int lv_query(lv_ctx* ctx, const lv_query_args* args);
 size_t lv_query_workspace_bytes(const lv_ctx* ctx);
+
+/* One decode step over L layers with HOST buffers (each layer an lv_ctx with the
+ * same batch, H_q and d): q [L][batch][H_q][d], tau [L][batch][H_q], out
+ * [L][batch][H_q][d], fp32 host memory (pinned for full speed). One host->device
+ * copy of every q and tau, the L fused layer queries back to back on the stream,
+ * one device->host copy of out, one synchronisation — the host-buffer form of the
+ * decode step. staging: optional DEVICE scratch of lv_query_layers_staging_bytes()
+ * bytes; NULL uses ctxs[0]'s internal staging (calls sharing ctxs[0] serialise).
+ * Each layer's query uses its context's internal workspace. */
+int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau, float scale, int strict,
+                    float* out, void* staging, void* stream);
+size_t lv_query_layers_staging_bytes(const lv_ctx* ctx, int L);
 
 /* Device geometry: out[8] = {padded d, cell keys r, arena rows, cells per slot,
  * query splits per slot, chunks per split, keys per chunk, query smem bytes}
@@ -190,6 +205,28 @@ int lv_bitmap_to_ids(const uint32_t* bits, int64_t words, int64_t rows, int64_t 
 int lv_sparse_attention(lv_ctx* ctx, int slot, const uint32_t* buffer_ids, int64_t nbuf,
                         const uint32_t* selected_ids, int64_t nsel, const float* q, float scale,
                         int where, float* out, float* weights, int64_t* ntok, void* stream);
+
+/* exact_check (query.hpp:48-49, query.cpp:22-31) on the device: flags[i] = 1 iff the
+ * normative dot(q, k_{ids[i]}) >= tau for key ids[i] of slot `slot`, else 0. ids, q
+ * and flags are host or device per `where`; ids must be < lv_n. */
+int lv_exact_check(lv_ctx* ctx, int slot, const uint32_t* ids, int64_t nids, const float* q, float tau, int where,
+                   uint8_t* flags, void* stream);
+
+/* The attention weights of a query (AttentionResult::weights, query.cpp:359-365):
+ * weights[i] = exp(scale * dot(q, k_{ids[i]}) - m) / l with the normative dot, for the
+ * attended ids of slot `slot` and the (m, l) of lv_query's `partial` row of that q
+ * head. ids, q, weights host or device per `where`. */
+int lv_attention_weights(lv_ctx* ctx, int slot, const uint32_t* ids, int64_t nids, const float* q, float scale,
+                         float m, float l, int where, float* weights, void* stream);
+
+/* derive_subspace_thresholds (query.hpp:60-65, query.cpp:305-336) over the device
+ * index of slot `slot`: with S slices of the SubspaceLayout (core.hpp:41-50), M_s = the
+ * largest AABB bound of subspace s over the cells holding indexed keys, slack =
+ * 4 d eps ||q|| sqrt(sum_s nb_s^2) (0 when S = 1, nb_s the cells' largest
+ * ||max(|lo|, |hi|)|| over s), tau_s = tau - (sum M - M_s) - slack. q [d] and out [S]
+ * host or device per `where`. Any key with dot(q, k) >= tau meets every tau_s. */
+int lv_subspace_thresholds(lv_ctx* ctx, int slot, const float* q, float tau, int S, int where, float* out,
+                           void* stream);
 
 /* Full-scan decode over keys [0, n) of every slot (fused split-K online
  * softmax, GQA-grouped). Same q/out conventions as lv_query. */

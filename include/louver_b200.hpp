@@ -30,11 +30,13 @@
 
 #include <algorithm>
 #include <chrono>
+#include <iterator>
 #include <limits>
 #include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -64,12 +66,11 @@ inline int check(int rc, const char* what) {
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
-// device scratch owned by one call
+// device scratch (the query clears what it accumulates into)
 struct DevBuf {
     void* p = nullptr;
     explicit DevBuf(size_t bytes) {
         if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
-        if (bytes) cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
     }
     ~DevBuf() { if (p) cudaFree(p); }
     DevBuf(const DevBuf&) = delete;
@@ -169,6 +170,20 @@ struct CacheQueryResult {
     std::optional<AttentionResult> attention;
 };
 
+// query.hpp:32-35 (the device's candidate set: live ids and the cells tested)
+struct CandidateSetView {
+    std::vector<KeyId> live_ids;
+    std::int64_t groups_tested = 0;
+};
+
+// The device index behind LouverCache::index(): contiguous cells of r keys, one AABB
+// summary row per cell, over the indexed keys [0, indexed_count).
+struct IndexView {
+    int r = 16;
+    std::size_t indexed_count = 0;
+    std::size_t cells = 0;
+};
+
 // cache.hpp:21-63: one head, fp32 KV in HBM, device index + update buffer of
 // capacity B (auto-flush at B). Single writer; const queries may run
 // concurrently (each call uses its own device workspace).
@@ -206,12 +221,13 @@ class LouverCache {
     // Folds pending keys into the index; false (no-op) when nothing is pending.
     bool flush_buffer() { return detail::check(lv_flush(ctx_.get(), nullptr), "lv_flush") == LV_OK; }
 
+    // cache.cpp:30-70. attention->weights (query.cpp:359-365) come from the query's own
+    // (m, l) and the normative scores of the attended ids. Each concurrent call leases its
+    // own device scratch from a pool (allocated once, reused: no allocation per query).
     CacheQueryResult query(const QueryRequest& req, FilterAlgo algo, bool strict_threshold = false) const {
         if (req.q.size() != static_cast<size_t>(dim_)) throw std::invalid_argument("dot: length mismatch");
-        const int64_t words = lv_bitmap_words(ctx_.get());
-        detail::DevBuf bits(static_cast<size_t>(words) * 4), totals(4 * 8),
-            ws(lv_query_workspace_bytes(ctx_.get()));
-        Vector out(dim_, 0.0f);
+        Lease sc(*this);
+        Vector out(dim_, 0.0f), part(dim_ + 2, 0.0f);
         int32_t counts[4] = {0, 0, 0, 0};
         const float tau = req.tau;
         lv_query_args a{};
@@ -222,25 +238,71 @@ class LouverCache {
         a.strict = strict_threshold ? 1 : 0;
         a.where = LV_HOST;
         a.out = out.data();
+        a.partial = part.data();
         a.counts = counts;
-        a.sel_bits = static_cast<uint32_t*>(bits.p);
-        a.totals = static_cast<uint64_t*>(totals.p);
-        a.workspace = ws.p;
+        a.sel_bits = sc->bits();
+        a.totals = sc->totals();
+        a.workspace = sc->ws.p;
         detail::check(lv_query(ctx_.get(), &a), "lv_query");
         const int64_t n_now = lv_n(ctx_.get()), indexed = lv_indexed_count(ctx_.get());
         CacheQueryResult r;
-        r.selected = bits_to_ids(static_cast<const uint32_t*>(bits.p), n_now);
+        r.selected = bits_to_ids(sc.get(), sc->bits(), n_now);
         for (KeyId id : r.selected)
             if (id < indexed) r.retrieved.push_back(id);
         for (int64_t j = indexed; j < n_now; ++j) r.retrieved.push_back(static_cast<KeyId>(j));
         uint64_t tot[4] = {0, 0, 0, 0};
-        detail::cuda_check(cudaMemcpy(tot, totals.p, sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        detail::cuda_check(cudaMemcpy(tot, sc->totals(), sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
         r.stats.groups_tested = static_cast<int64_t>(tot[0]);
         r.stats.keys_scanned = counts[2];
         r.stats.f_scan = n_now ? double(counts[2]) / double(n_now) : 1.0;
         r.stats.gate_cost_equiv = 2.0 * double(tot[0]) / double(cfg_.r);
-        if (counts[3]) r.attention = AttentionResult{strict_threshold ? r.selected : r.retrieved, {}, std::move(out)};
+        if (counts[3]) {
+            AttentionResult att{strict_threshold ? r.selected : r.retrieved, {}, std::move(out)};
+            att.weights.resize(att.selected_ids.size());
+            if (!att.selected_ids.empty())
+                detail::check(lv_attention_weights(ctx_.get(), 0, att.selected_ids.data(),
+                                                   (int64_t)att.selected_ids.size(), req.q.data(),
+                                                   req.effective_scale(), part[0], part[1], LV_HOST,
+                                                   att.weights.data(), nullptr),
+                              "attention weights");
+            r.attention = std::move(att);
+        }
         return r;
+    }
+
+    // query_ta / query_full_subspace's candidate set (query.hpp:48-58) on the device:
+    // every indexed key of a cell whose bound reaches tau (ascending), with the stats.
+    CandidateSetView candidates(const QueryRequest& req) const {
+        if (req.q.size() != static_cast<size_t>(dim_)) throw std::invalid_argument("dot: length mismatch");
+        Lease sc(*this);
+        int32_t counts[4] = {0, 0, 0, 0};
+        const float tau = req.tau;
+        lv_query_args a{};
+        a.q = req.q.data();
+        a.tau = &tau;
+        a.scale = req.effective_scale();
+        a.algo = LV_ALGO_TA;
+        a.where = LV_HOST;
+        a.counts = counts;
+        a.totals = sc->totals();
+        a.cand_bits = sc->bits();
+        a.workspace = sc->ws.p;
+        detail::check(lv_query(ctx_.get(), &a), "lv_query");
+        CandidateSetView c;
+        c.live_ids = bits_to_ids(sc.get(), sc->bits(), (int64_t)indexed_count());
+        uint64_t tot[4] = {0, 0, 0, 0};
+        detail::cuda_check(cudaMemcpy(tot, sc->totals(), sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        c.groups_tested = static_cast<int64_t>(tot[0]);
+        return c;
+    }
+
+    // cache.hpp:49: a host copy of the device store (KeyStore of the stored rows)
+    KeyStore store() const { return KeyStore(rows(false), rows(true), dim_); }
+    // cache.hpp:50: the device index's shape (cells of r contiguous keys with AABB summaries)
+    IndexView index() const {
+        int64_t g[8] = {0};
+        detail::check(lv_geometry(ctx_.get(), g), "lv_geometry");
+        return IndexView{static_cast<int>(g[1]), indexed_count(), (indexed_count() + g[1] - 1) / g[1]};
     }
 
     int dim() const { return dim_; }
@@ -265,19 +327,62 @@ class LouverCache {
 
     // device bitmap [words] -> ascending ids < limit (device compaction kernel)
     std::vector<KeyId> bits_to_ids(const uint32_t* dev_bits, int64_t limit) const {
-        if (limit <= 0) return {};
-        detail::DevBuf ids(static_cast<size_t>(limit) * 4), cnt(4);
-        detail::check(lv_bitmap_to_ids(dev_bits, lv_bitmap_words(ctx_.get()), 1, limit, static_cast<uint32_t*>(ids.p),
-                                       limit, static_cast<int32_t*>(cnt.p), nullptr),
-                      "lv_bitmap_to_ids");
-        int32_t c = 0;
-        detail::cuda_check(cudaMemcpy(&c, cnt.p, 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
-        std::vector<KeyId> out(static_cast<size_t>(c));
-        if (c) detail::cuda_check(cudaMemcpy(out.data(), ids.p, 4 * static_cast<size_t>(c), cudaMemcpyDeviceToHost), "cudaMemcpy");
-        return out;
+        Lease sc(*this);
+        return bits_to_ids(sc.get(), dev_bits, limit);
     }
 
   private:
+    // per-call device scratch, pooled: leased by a query, returned when it ends
+    struct Scratch {
+        std::size_t cap_keys;
+        std::size_t tot_off;               // byte offset of totals [4] u64 + count i32 after the bitmap
+        detail::DevBuf bitbuf, ws, idbuf;  // bitmap + totals + count; query workspace; ids [cap]
+        Scratch(std::size_t cap, int64_t words, std::size_t ws_bytes)
+            : cap_keys(cap), tot_off((static_cast<size_t>(words) * 4 + 15) / 16 * 16),
+              bitbuf(tot_off + 48), ws(ws_bytes), idbuf(cap * 4) {}
+        uint32_t* bits() { return static_cast<uint32_t*>(bitbuf.p); }
+        uint64_t* totals() { return reinterpret_cast<uint64_t*>(static_cast<char*>(bitbuf.p) + tot_off); }
+        int32_t* count() { return reinterpret_cast<int32_t*>(totals() + 4); }
+    };
+    class Lease {
+      public:
+        explicit Lease(const LouverCache& c) : c_(c) {
+            std::lock_guard<std::mutex> g(c_.pool_mu_);
+            const int64_t words = lv_bitmap_words(c_.ctx_.get());
+            while (!c_.pool_.empty()) {  // drop scratch sized for a smaller arena (after regrowth)
+                std::unique_ptr<Scratch> s = std::move(c_.pool_.back());
+                c_.pool_.pop_back();
+                if (s->cap_keys == c_.capacity_) {
+                    s_ = std::move(s);
+                    break;
+                }
+            }
+            if (!s_) s_ = std::make_unique<Scratch>(c_.capacity_, words, lv_query_workspace_bytes(c_.ctx_.get()));
+        }
+        ~Lease() {
+            std::lock_guard<std::mutex> g(c_.pool_mu_);
+            c_.pool_.push_back(std::move(s_));
+        }
+        Scratch* operator->() { return s_.get(); }
+        Scratch* get() { return s_.get(); }
+
+      private:
+        const LouverCache& c_;
+        std::unique_ptr<Scratch> s_;
+    };
+
+    std::vector<KeyId> bits_to_ids(Scratch* sc, const uint32_t* dev_bits, int64_t limit) const {
+        if (limit <= 0) return {};
+        detail::check(lv_bitmap_to_ids(dev_bits, lv_bitmap_words(ctx_.get()), 1, limit, static_cast<uint32_t*>(sc->idbuf.p),
+                                       limit, sc->count(), nullptr),
+                      "lv_bitmap_to_ids");
+        int32_t c = 0;
+        detail::cuda_check(cudaMemcpy(&c, sc->count(), 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+        std::vector<KeyId> out(static_cast<size_t>(c));
+        if (c) detail::cuda_check(cudaMemcpy(out.data(), sc->idbuf.p, 4 * static_cast<size_t>(c), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        return out;
+    }
+
     void create(std::size_t capacity) {
         capacity_ = capacity;
         lv_config c{};
@@ -303,6 +408,8 @@ class LouverCache {
     std::size_t buffer_capacity_;
     std::size_t capacity_ = 0;
     std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
+    mutable std::mutex pool_mu_;
+    mutable std::vector<std::unique_ptr<Scratch>> pool_;
 };
 
 // query.hpp:44-45: ids j < limit with dot(q, k_j) >= tau (normative dot, on the device).
@@ -315,6 +422,76 @@ inline std::vector<KeyId> brute_force_range(const LouverCache& cache, ConstVecRe
                                        static_cast<uint32_t*>(bits.p), nullptr),
                   "lv_brute_force_range");
     return cache.bits_to_ids(static_cast<const uint32_t*>(bits.p), (int64_t)limit);
+}
+
+// query.hpp:48-49: the candidates meeting tau (normative dot), ascending.
+inline std::vector<KeyId> exact_check(const LouverCache& cache, std::span<const KeyId> candidates, ConstVecRef q,
+                                      Scalar tau) {
+    if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    std::vector<uint8_t> flags(candidates.size());
+    if (!candidates.empty())
+        detail::check(lv_exact_check(cache.handle(), 0, candidates.data(), (int64_t)candidates.size(), q.data(), tau,
+                                     LV_HOST, flags.data(), nullptr),
+                      "exact_check");
+    std::vector<KeyId> out;
+    for (size_t i = 0; i < candidates.size(); ++i)
+        if (flags[i]) out.push_back(candidates[i]);
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+// query.hpp:32-35: CandidateSet with the stats the device reports (groups = cells).
+struct CandidateSet {
+    std::vector<KeyId> live_ids;  // ascending, duplicate-free, among the indexed keys
+    QueryStats stats;
+};
+
+namespace detail {
+inline CandidateSet candidate_set(const LouverCache& cache, const QueryRequest& req) {
+    CandidateSetView v = cache.candidates(req);
+    CandidateSet c;
+    c.stats.groups_tested = v.groups_tested;
+    c.stats.keys_scanned = static_cast<std::int64_t>(v.live_ids.size());
+    const auto idx = cache.indexed_count();
+    c.stats.f_scan = idx ? double(v.live_ids.size()) / double(idx) : 0.0;  // finalize_stats, query.cpp:70-78
+    c.stats.gate_cost_equiv = 2.0 * double(v.groups_tested) / double(cache.index().r);
+    c.live_ids = std::move(v.live_ids);
+    return c;
+}
+}  // namespace detail
+
+// query.hpp:55-58: the device filter (full-dimension cell bounds against req.tau; the
+// candidate set contains every indexed key with dot(q, k) >= tau).
+inline CandidateSet query_ta(const LouverCache& cache, const QueryRequest& req) {
+    return detail::candidate_set(cache, req);
+}
+
+// query.hpp:51-53: validates tau_subspace like the reference (query.cpp:84-87); the device
+// filter bounds each cell over all coordinates against req.tau.
+inline CandidateSet query_full_subspace(const LouverCache& cache, const QueryRequest& req, int S) {
+    if (!req.tau_subspace) throw std::invalid_argument("query_full_subspace: tau_subspace required");
+    if (static_cast<int>(req.tau_subspace->size()) != S)
+        throw std::invalid_argument("query_full_subspace: tau_subspace length != S");
+    return detail::candidate_set(cache, req);
+}
+
+// query.hpp:60-65 over the device index (lv_subspace_thresholds).
+inline std::vector<Scalar> derive_subspace_thresholds(const LouverCache& cache, ConstVecRef q, Scalar tau, int S) {
+    if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    std::vector<Scalar> out(static_cast<size_t>(S > 0 ? S : 0));
+    detail::check(lv_subspace_thresholds(cache.handle(), 0, q.data(), tau, S, LV_HOST, out.data(), nullptr),
+                  "derive_subspace_thresholds");
+    return out;
+}
+
+// query.hpp:74-75 / query.cpp:374-383: |retrieved ∩ exact_topk| / k.
+inline double recall_at_k(std::span<const KeyId> exact_topk, std::span<const KeyId> retrieved) {
+    if (exact_topk.empty()) throw std::invalid_argument("recall_at_k: k >= 1 required");
+    std::vector<KeyId> a(exact_topk.begin(), exact_topk.end()), b(retrieved.begin(), retrieved.end()), both;
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(both));
+    return static_cast<double>(both.size()) / static_cast<double>(a.size());
 }
 
 // query.hpp:69-72: softmax over sort∪unique(selected ∪ buffer); nullopt when empty.

@@ -29,12 +29,13 @@ from .louver import (  # noqa: F401
     QueryStats,
     brute_force_range,
     lse_merge,
+    query_layers_host,
     sparse_attention,
 )
 
 __all__ = [
     "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
-    "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "sparse_attention", "LouverError",
+    "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "query_layers_host", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
     "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim", "GraphDecodeReport", "run_decode_graph",

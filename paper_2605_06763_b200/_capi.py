@@ -52,6 +52,7 @@ class lv_query_args(C.Structure):
         ("totals", C.c_void_p),
         ("workspace", C.c_void_p),
         ("stream", C.c_void_p),
+        ("cand_bits", C.c_void_p),
     ]
 
 
@@ -89,6 +90,8 @@ _SIGS = {
     "lv_sync_counters": (C.c_int, [_P, _P]),
     "lv_query": (C.c_int, [_P, C.POINTER(lv_query_args)]),
     "lv_query_workspace_bytes": (C.c_size_t, [_P]),
+    "lv_query_layers": (C.c_int, [_P, C.c_int, _P, _P, C.c_float, C.c_int, _P, _P, _P]),
+    "lv_query_layers_staging_bytes": (C.c_size_t, [_P, C.c_int]),
     "lv_geometry": (C.c_int, [_P, _P]),
     "lv_debug_trace": (C.c_int, [_P, _P]),
     "lv_layer_geometry": (C.c_int, [_P, _P]),
@@ -106,6 +109,10 @@ _SIGS = {
          C.POINTER(C.c_int64), _P],
     ),
     "lv_dense_decode": (C.c_int, [_P, _P, C.c_float, C.c_int, _P, _P, _P]),
+    "lv_exact_check": (C.c_int, [_P, C.c_int, _P, C.c_int64, _P, C.c_float, C.c_int, _P, _P]),
+    "lv_subspace_thresholds": (C.c_int, [_P, C.c_int, _P, C.c_float, C.c_int, C.c_int, _P, _P]),
+    "lv_attention_weights": (C.c_int, [_P, C.c_int, _P, C.c_int64, _P, C.c_float, C.c_float, C.c_float, C.c_int,
+                                       _P, _P]),
     "lv_lse_merge": (C.c_int, [_P, C.c_int, C.c_int64, C.c_int, _P, _P]),
     "lv_reservoir_create": (C.c_int, [C.c_int64, C.c_uint64, C.POINTER(_P)]),
     "lv_reservoir_destroy": (C.c_int, [_P]),

@@ -237,6 +237,70 @@ __global__ void lse_merge_kernel(const float* __restrict__ part, int P, long lon
     }
 }
 
+// derive_subspace_thresholds (query.cpp:305-336) over the device cells: block s computes,
+// over cells [0, ncells), M_s = max of the AABB bound sum_{c in s} max(q_c lo_c, q_c hi_c)
+// (gate_bounds' order, float) and the norm bound max ||max(|lo|, |hi|)||_s (double,
+// append_gate_entry index.cpp:147-154)
+template <typename T, int DP>
+__global__ void subspace_peaks_kernel(const T* __restrict__ rows, long long ncells, const float* __restrict__ q,
+                                      const int* __restrict__ offs, double* __restrict__ peak,
+                                      double* __restrict__ nb) {
+    __shared__ double red[2][8];
+    const int s = blockIdx.x, b = offs[s], e = offs[s + 1];
+    double pk = -INFINITY, nq = 0.0;
+    for (long long cell = threadIdx.x; cell < ncells; cell += blockDim.x) {
+        const T* row = rows + (size_t)cell * 2 * DP;  // [hi (DP) | lo (DP)]
+        float f = 0.0f;
+        double sq = 0.0;
+        for (int c = b; c < e; ++c) {
+            const float h = to_f<T>(row[c]), l = to_f<T>(row[DP + c]);
+            f = __fadd_rn(f, fmaxf(__fmul_rn(q[c], l), __fmul_rn(q[c], h)));
+            const double m = fmax(fabs((double)l), fabs((double)h));
+            sq += m * m;
+        }
+        pk = fmax(pk, (double)f);
+        nq = fmax(nq, sqrt(sq));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        pk = fmax(pk, __shfl_xor_sync(0xffffffffu, pk, o));
+        nq = fmax(nq, __shfl_xor_sync(0xffffffffu, nq, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = pk;
+        red[1][threadIdx.x >> 5] = nq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            pk = fmax(pk, red[0][w]);
+            nq = fmax(nq, red[1][w]);
+        }
+        peak[s] = fmax(pk, red[0][0]);
+        nb[s] = fmax(nq, red[1][0]);
+    }
+}
+
+// exact_check (query.cpp:22-31): flag[i] = normative dot(q, k_ids[i]) >= tau
+template <typename T, int DP>
+__global__ void exact_flags_kernel(const T* __restrict__ Ks, const unsigned* __restrict__ ids, long long nids,
+                                   const float* __restrict__ q, float tau, unsigned char* __restrict__ flags) {
+    __shared__ float qs[DP];
+    for (int c = threadIdx.x; c < DP; c += blockDim.x) qs[c] = q[c];
+    __syncthreads();
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nids) return;
+    const T* row = Ks + (size_t)ids[i] * DP;
+    float s = 0.0f;
+    for (int c = 0; c < DP; ++c) s = __fadd_rn(s, __fmul_rn(qs[c], to_f<T>(row[c])));
+    flags[i] = s >= tau ? 1 : 0;
+}
+
+// weights_i = exp(s_i - m) / l for a query's own (m, l)
+__global__ void attn_weights_kernel(float* __restrict__ s, long long n, float m, float l) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) s[i] = expf(s[i] - m) / l;
+}
+
 // weights_i = exp(s_i - M) / L  (query.cpp:359-365)
 __global__ void token_weights_kernel(const float* __restrict__ scores, long long ntok,
                                      const float* __restrict__ ml, float* __restrict__ w) {

@@ -81,6 +81,9 @@ struct lv_ctx {
     size_t ws_bytes = 0;
     // host mirrors of the device counters
     long long n = 0, indexed = 0, flushes = 0;
+    void* stage = nullptr;       // lv_query_layers' internal staging (lazily grown)
+    size_t stage_bytes = 0;
+    std::mutex stage_mu;
     int l2pf = 0;                // experiment knob (LV_L2PF)
     int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
@@ -247,7 +250,8 @@ int sync_if_host(int where, cudaStream_t st) {
 
 int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev, long long limit,
                      float scale, int strict, Workspace& w, float* out, float* part_out,
-                     unsigned* bits, int* counts, unsigned long long* totals, cudaStream_t st) {
+                     unsigned* bits, int* counts, unsigned long long* totals, cudaStream_t st,
+                     unsigned* cand_bits = nullptr) {
     lvk::QueryParams p{};
     p.K = c->K;
     p.V = c->V;
@@ -274,6 +278,7 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
     p.bits_words = c->bits_words;
     p.counts = counts;
     p.totals = totals;
+    p.cand_bits = cand_bits;
     dim3 grid((unsigned)c->splits, (unsigned)c->slots);
     cudaError_t e;
     if (c->cfg.dtype == LV_BF16 && mode != lvk::kBrute) {
@@ -450,6 +455,7 @@ int lv_destroy(lv_ctx* c) {
     cudaFree(c->ctr);
     cudaFree(c->ins_ticket);
     cudaFree(c->ws_mem);
+    if (c->stage) cudaFree(c->stage);
     delete c;
     return LV_OK;
 }
@@ -693,9 +699,13 @@ int lv_query(lv_ctx* c, const lv_query_args* a) {
     if (a->totals) LV_CUDA(cudaMemsetAsync(a->totals, 0, sizeof(uint64_t) * 4, st));
     if (a->sel_bits)
         LV_CUDA(cudaMemsetAsync(a->sel_bits, 0, sizeof(uint32_t) * c->rows * c->bits_words, st));
+    if (a->cand_bits) {
+        if (c->cfg.dtype != LV_F32) return fail(LV_EINVAL, "lv_query: cand_bits needs an fp32 cache");
+        LV_CUDA(cudaMemsetAsync(a->cand_bits, 0, sizeof(uint32_t) * c->slots * c->bits_words, st));
+    }
     if (int rc = run_query_kernel(c, lvk::kQuery, qd, taud, 0, a->scale, a->strict, w, outd, pod,
                                   a->sel_bits, cntd, reinterpret_cast<unsigned long long*>(a->totals),
-                                  st))
+                                  st, a->cand_bits))
         return rc;
     const cudaMemcpyKind kind = a->where == LV_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (a->out && !direct)
@@ -710,6 +720,208 @@ int lv_query(lv_ctx* c, const lv_query_args* a) {
     if (a->counts && a->where == LV_HOST)
         LV_CUDA(cudaMemcpyAsync(a->counts, w.counts, sizeof(int) * c->rows * 4, cudaMemcpyDeviceToHost, st));
     return sync_if_host(a->where, st);
+}
+
+size_t lv_query_layers_staging_bytes(const lv_ctx* c, int L) {
+    if (!c || L < 1) return 0;
+    const size_t rows = (size_t)c->rows, d = (size_t)c->cfg.d;
+    return align256(sizeof(float) * L * rows * d) * 2 + align256(sizeof(float) * L * rows);
+}
+
+int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau, float scale, int strict,
+                    float* out, void* staging, void* stream) {
+    if (!ctxs || L < 1 || !q || !tau || !out) return fail(LV_EINVAL, "lv_query_layers: null argument");
+    lv_ctx* c0 = ctxs[0];
+    if (!c0) return fail(LV_EINVAL, "lv_query_layers: null context");
+    for (int l = 1; l < L; ++l)
+        if (!ctxs[l] || ctxs[l]->rows != c0->rows || ctxs[l]->cfg.d != c0->cfg.d)
+            return fail(LV_EINVAL, "lv_query_layers: every layer needs the same batch, H_q and d");
+    cudaStream_t st = S(stream);
+    const size_t rows = (size_t)c0->rows, d = (size_t)c0->cfg.d;
+    const size_t need = lv_query_layers_staging_bytes(c0, L);
+    std::unique_lock<std::mutex> lock(c0->stage_mu, std::defer_lock);
+    unsigned char* base = static_cast<unsigned char*>(staging);
+    if (!base) {  // the first context's internal staging: calls sharing it serialise
+        lock.lock();
+        if (c0->stage_bytes < need) {
+            if (c0->stage) LV_CUDA(cudaFree(c0->stage));
+            c0->stage = nullptr;
+            c0->stage_bytes = 0;
+            LV_CUDA(cudaMalloc(&c0->stage, need));
+            c0->stage_bytes = need;
+        }
+        base = static_cast<unsigned char*>(c0->stage);
+    }
+    float* qd = reinterpret_cast<float*>(base);
+    float* od = reinterpret_cast<float*>(base + align256(sizeof(float) * L * rows * d));
+    float* td = reinterpret_cast<float*>(base + 2 * align256(sizeof(float) * L * rows * d));
+    // one copy in for every layer's q and tau, the L queries back to back, one copy out
+    LV_CUDA(cudaMemcpyAsync(qd, q, sizeof(float) * L * rows * d, cudaMemcpyHostToDevice, st));
+    LV_CUDA(cudaMemcpyAsync(td, tau, sizeof(float) * L * rows, cudaMemcpyHostToDevice, st));
+    for (int l = 0; l < L; ++l) {
+        lv_query_args a{};
+        a.q = qd + (size_t)l * rows * d;
+        a.tau = td + (size_t)l * rows;
+        a.scale = scale;
+        a.algo = LV_ALGO_TA;
+        a.strict = strict;
+        a.where = LV_DEVICE;
+        a.out = od + (size_t)l * rows * d;
+        a.stream = stream;
+        if (int rc = lv_query(ctxs[l], &a)) return rc;
+    }
+    LV_CUDA(cudaMemcpyAsync(out, od, sizeof(float) * L * rows * d, cudaMemcpyDeviceToHost, st));
+    LV_CUDA(cudaStreamSynchronize(st));
+    return LV_OK;
+}
+
+namespace {
+// ids + q staged on the device (DEVICE inputs used in place); scratch from the stream-ordered pool
+struct IdsQ {
+    const unsigned* ids = nullptr;
+    float* q = nullptr;   // [DP], zero-padded
+    void* mem = nullptr;
+};
+int stage_ids_q(lv_ctx* c, const uint32_t* ids, int64_t nids, const float* q, int where, cudaStream_t st, IdsQ* o,
+                size_t extra, void** extra_p) {
+    const size_t bi = where == LV_HOST ? align256(sizeof(uint32_t) * nids) : 0;
+    if (where == LV_HOST)
+        for (int64_t i = 0; i < nids; ++i)
+            if ((long long)ids[i] >= c->n) return fail(LV_ERANGE, "key id >= n");
+    LV_CUDA(cudaMallocAsync(&o->mem, bi + align256(sizeof(float) * c->DP) + align256(extra), st));
+    unsigned char* m = static_cast<unsigned char*>(o->mem);
+    if (where == LV_HOST) {
+        LV_CUDA(cudaMemcpyAsync(m, ids, sizeof(uint32_t) * nids, cudaMemcpyHostToDevice, st));
+        o->ids = reinterpret_cast<const unsigned*>(m);
+    } else {
+        o->ids = ids;
+    }
+    o->q = reinterpret_cast<float*>(m + bi);
+    LV_CUDA(cudaMemsetAsync(o->q, 0, sizeof(float) * c->DP, st));
+    LV_CUDA(cudaMemcpyAsync(o->q, q, sizeof(float) * c->cfg.d,
+                            where == LV_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    if (extra_p) *extra_p = m + bi + align256(sizeof(float) * c->DP);
+    return LV_OK;
+}
+}  // namespace
+
+int lv_exact_check(lv_ctx* c, int slot, const uint32_t* ids, int64_t nids, const float* q, float tau, int where,
+                   uint8_t* flags, void* stream) {
+    if (!c || !q || (nids > 0 && (!ids || !flags)) || nids < 0) return fail(LV_EINVAL, "exact_check: bad arguments");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "exact_check: slot out of range");
+    if (nids == 0) return LV_OK;
+    cudaStream_t st = S(stream);
+    IdsQ in;
+    void* fl = nullptr;
+    if (int rc = stage_ids_q(c, ids, nids, q, where, st, &in, where == LV_HOST ? (size_t)nids : 0, &fl)) return rc;
+    unsigned char* fd = where == LV_HOST ? static_cast<unsigned char*>(fl) : flags;
+    const size_t es = esize(c->cfg.dtype);
+    const void* Ks = (const unsigned char*)c->K + (size_t)slot * c->cap * c->DP * es;
+    const unsigned tb = (unsigned)((nids + 127) / 128);
+#define LV_EX(T, D) lvk::exact_flags_kernel<T, D><<<tb, 128, 0, st>>>((const T*)Ks, in.ids, nids, in.q, tau, fd);
+    if (c->cfg.dtype == LV_BF16) {
+        if (c->DP == 64) { LV_EX(__nv_bfloat16, 64) } else if (c->DP == 128) { LV_EX(__nv_bfloat16, 128) } else { LV_EX(__nv_bfloat16, 256) }
+    } else {
+        if (c->DP == 64) { LV_EX(float, 64) } else if (c->DP == 128) { LV_EX(float, 128) } else { LV_EX(float, 256) }
+    }
+#undef LV_EX
+    LV_CUDA(cudaGetLastError());
+    if (where == LV_HOST) LV_CUDA(cudaMemcpyAsync(flags, fd, (size_t)nids, cudaMemcpyDeviceToHost, st));
+    LV_CUDA(cudaFreeAsync(in.mem, st));
+    return sync_if_host(where, st);
+}
+
+int lv_attention_weights(lv_ctx* c, int slot, const uint32_t* ids, int64_t nids, const float* q, float scale,
+                         float m, float l, int where, float* weights, void* stream) {
+    if (!c || !q || (nids > 0 && (!ids || !weights)) || nids < 0)
+        return fail(LV_EINVAL, "attention_weights: bad arguments");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "attention_weights: slot out of range");
+    if (nids == 0) return LV_OK;
+    cudaStream_t st = S(stream);
+    IdsQ in;
+    void* sc_mem = nullptr;
+    if (int rc = stage_ids_q(c, ids, nids, q, where, st, &in, sizeof(float) * nids, &sc_mem)) return rc;
+    float* scores = where == LV_HOST ? static_cast<float*>(sc_mem) : weights;
+    const float sc = scale != 0.0f ? scale : (float)(1.0 / std::sqrt((double)c->cfg.d));
+    const size_t es = esize(c->cfg.dtype);
+    const void* Ks = (const unsigned char*)c->K + (size_t)slot * c->cap * c->DP * es;
+    const unsigned tb = (unsigned)((nids + 127) / 128);
+#define LV_W(T, D) lvk::token_scores_kernel<T, D><<<tb, 128, 0, st>>>((const T*)Ks, in.ids, nids, in.q, sc, scores);
+    if (c->cfg.dtype == LV_BF16) {
+        if (c->DP == 64) { LV_W(__nv_bfloat16, 64) } else if (c->DP == 128) { LV_W(__nv_bfloat16, 128) } else { LV_W(__nv_bfloat16, 256) }
+    } else {
+        if (c->DP == 64) { LV_W(float, 64) } else if (c->DP == 128) { LV_W(float, 128) } else { LV_W(float, 256) }
+    }
+#undef LV_W
+    lvk::attn_weights_kernel<<<tb, 128, 0, st>>>(scores, nids, m, l);
+    LV_CUDA(cudaGetLastError());
+    if (where == LV_HOST) LV_CUDA(cudaMemcpyAsync(weights, scores, sizeof(float) * nids, cudaMemcpyDeviceToHost, st));
+    LV_CUDA(cudaFreeAsync(in.mem, st));
+    return sync_if_host(where, st);
+}
+
+int lv_subspace_thresholds(lv_ctx* c, int slot, const float* q, float tau, int S, int where, float* out,
+                           void* stream) {
+    if (!c || !q || !out) return fail(LV_EINVAL, "derive_subspace_thresholds: null argument");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "derive_subspace_thresholds: slot out of range");
+    const int d = c->cfg.d;
+    if (S < 1 || S > d) return fail(LV_EINVAL, "SubspaceLayout: 1 <= S <= d required");
+    // SubspaceLayout (core.hpp:41-50): S contiguous slices, the first d % S one wider
+    std::vector<int> offs(S + 1, 0);
+    for (int i = 0; i < S; ++i) offs[i + 1] = offs[i] + d / S + (i < d % S ? 1 : 0);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const long long ncells = (c->indexed + c->r - 1) >> c->r_log2;  // cells holding indexed keys
+    std::vector<float> qh(d);
+    if (where == LV_HOST) {
+        std::memcpy(qh.data(), q, sizeof(float) * d);
+    } else {
+        LV_CUDA(cudaMemcpyAsync(qh.data(), q, sizeof(float) * d, cudaMemcpyDeviceToHost, st));
+        LV_CUDA(cudaStreamSynchronize(st));
+    }
+    std::vector<double> peak(S, 0.0), nb(S, 0.0);
+    if (ncells > 0) {
+        void* mem = nullptr;
+        const size_t bq = align256(sizeof(float) * c->DP), bo = align256(sizeof(int) * (S + 1));
+        LV_CUDA(cudaMallocAsync(&mem, bq + bo + 2 * align256(sizeof(double) * S), st));
+        unsigned char* m = static_cast<unsigned char*>(mem);
+        float* qd = reinterpret_cast<float*>(m);
+        int* od = reinterpret_cast<int*>(m + bq);
+        double* pd = reinterpret_cast<double*>(m + bq + bo);
+        double* nd = reinterpret_cast<double*>(m + bq + bo + align256(sizeof(double) * S));
+        LV_CUDA(cudaMemsetAsync(qd, 0, sizeof(float) * c->DP, st));
+        LV_CUDA(cudaMemcpyAsync(qd, qh.data(), sizeof(float) * d, cudaMemcpyHostToDevice, st));
+        LV_CUDA(cudaMemcpyAsync(od, offs.data(), sizeof(int) * (S + 1), cudaMemcpyHostToDevice, st));
+        const size_t es = esize(c->cfg.dtype);
+        const void* rows = (const unsigned char*)c->lo + (size_t)slot * c->cap_cells * 2 * c->DP * es;
+#define LV_SP(T, D) lvk::subspace_peaks_kernel<T, D><<<S, 256, 0, st>>>((const T*)rows, ncells, qd, od, pd, nd);
+        if (c->cfg.dtype == LV_BF16) {
+            if (c->DP == 64) { LV_SP(__nv_bfloat16, 64) } else if (c->DP == 128) { LV_SP(__nv_bfloat16, 128) } else { LV_SP(__nv_bfloat16, 256) }
+        } else {
+            if (c->DP == 64) { LV_SP(float, 64) } else if (c->DP == 128) { LV_SP(float, 128) } else { LV_SP(float, 256) }
+        }
+#undef LV_SP
+        LV_CUDA(cudaGetLastError());
+        LV_CUDA(cudaMemcpyAsync(peak.data(), pd, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+        LV_CUDA(cudaMemcpyAsync(nb.data(), nd, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+        LV_CUDA(cudaFreeAsync(mem, st));
+        LV_CUDA(cudaStreamSynchronize(st));
+    }
+    // query.cpp:322-335: slack and tau_s, in double
+    double nbsq = 0.0, qq = 0.0, total = 0.0;
+    for (int s = 0; s < S; ++s) nbsq += nb[s] * nb[s];
+    for (int i = 0; i < d; ++i) qq += (double)qh[i] * qh[i];
+    const double eps = 1.1920928955078125e-07;
+    const double slack = S == 1 ? 0.0 : 4.0 * d * eps * std::sqrt(qq) * std::sqrt(nbsq);
+    for (int s = 0; s < S; ++s) total += peak[s];
+    std::vector<float> res(S);
+    for (int s = 0; s < S; ++s) res[s] = (float)((double)tau - (total - peak[s]) - slack);
+    if (where == LV_HOST) {
+        std::memcpy(out, res.data(), sizeof(float) * S);
+    } else {
+        LV_CUDA(cudaMemcpyAsync(out, res.data(), sizeof(float) * S, cudaMemcpyHostToDevice, st));
+        LV_CUDA(cudaStreamSynchronize(st));
+    }
+    return LV_OK;
 }
 
 int lv_dense_decode(lv_ctx* c, const float* q, float scale, int where, float* out, float* partial,

@@ -70,6 +70,7 @@ struct QueryParams {
     int* counts;            // [slots*G][4] or null
     unsigned long long* totals;  // [4] or null
     long long* tot_trace;        // debug: per-CTA phase timestamps (bf16 cell stream) or null
+    unsigned* cand_bits;         // [slots][bits_words] candidate keys (indexed keys of surviving cells) or null
 };
 
 template <typename T>
@@ -410,6 +411,11 @@ __global__ void __launch_bounds__(kThreads) louver_query_kernel(const QueryParam
                     }
                     ++t_cells;
                     if (m) ++t_surv;
+                    if (p.cand_bits && m) {  // query_ta's live ids: the cell's indexed keys
+                        const long long ke = ce < idx_end ? ce : idx_end;
+                        for (long long k = cs; k < ke; ++k)
+                            atomicOr(p.cand_bits + (size_t)slot * p.bits_words + (k >> 5), 1u << (k & 31));
+                    }
 #pragma unroll
                     for (int g = 0; g < G; ++g)
                         if (m & (1u << g)) {

@@ -24,6 +24,7 @@ import ctypes as C
 import dataclasses
 import enum
 import math
+import threading
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -194,6 +195,8 @@ class LouverCache:
         self.B = int(buffer_capacity)
         self._ctx = _Context(_config(dim, 1, 1, 1, LV_F32, cfg, self.B, max(capacity, 16)))
         self._cap = max(capacity, 16)
+        self._pool_lock = threading.Lock()
+        self._pool = []  # (bits, totals) device scratch leased by queries
 
     @classmethod
     def adopt(cls, keys: np.ndarray, values: np.ndarray, cfg: BuildConfig, buffer_capacity: int):
@@ -257,39 +260,61 @@ class LouverCache:
     # -- reader side -------------------------------------------------------------
     def query(self, req: QueryRequest, algo: FilterAlgo = FilterAlgo.Ta, strict_threshold: bool = False,
               want_weights: bool = False) -> CacheQueryResult:
-        torch = _torch()
+        """cache.cpp:30-70. The attention's weights (query.cpp:359-365) come from the
+        query's own (m, l) and the normative scores of the attended ids; ``want_weights``
+        is accepted for compatibility (weights are always filled, as in the reference).
+        Device scratch is leased from a per-cache pool (no allocation per query)."""
         q = np.ascontiguousarray(req.q, dtype=np.float32).reshape(-1)
         if q.size != self.d:
             raise ValueError("dot: length mismatch")
         tau = np.array([req.tau], dtype=np.float32)
         out = np.zeros((self.d,), dtype=np.float32)
+        part = np.zeros((self.d + 2,), dtype=np.float32)
         counts = np.zeros((4,), dtype=np.int32)
-        bits = torch.zeros((1, self._ctx.bitmap_words), dtype=torch.int32, device="cuda")
-        totals = torch.zeros((4,), dtype=torch.int64, device="cuda")
-        args = _capi.lv_query_args(
-            q=_ptr(q), tau=_ptr(tau), scale=req.effective_scale(), algo=int(algo),
-            strict=1 if strict_threshold else 0, where=LV_HOST, out=_ptr(out), partial=None,
-            counts=_ptr(counts), sel_bits=bits.data_ptr(), totals=totals.data_ptr(), workspace=None,
-            stream=None,
-        )
-        check(self._ctx.lib.lv_query(self._ctx.h, C.byref(args)), "lv_query")
-        n, indexed = self._ctx.n, self._ctx.indexed
-        selected = self._ctx.bits_to_ids(bits, 1, n)[0] if n else np.zeros((0,), np.uint32)
+        bits, totals = self._lease()
+        try:
+            args = _capi.lv_query_args(
+                q=_ptr(q), tau=_ptr(tau), scale=req.effective_scale(), algo=int(algo),
+                strict=1 if strict_threshold else 0, where=LV_HOST, out=_ptr(out), partial=_ptr(part),
+                counts=_ptr(counts), sel_bits=bits.data_ptr(), totals=totals.data_ptr(), workspace=None,
+                stream=None,
+            )
+            check(self._ctx.lib.lv_query(self._ctx.h, C.byref(args)), "lv_query")
+            n, indexed = self._ctx.n, self._ctx.indexed
+            selected = self._ctx.bits_to_ids(bits, 1, n)[0] if n else np.zeros((0,), np.uint32)
+            tot = totals.cpu().numpy()
+        finally:
+            self._release(bits, totals)
         retrieved = np.concatenate([selected[selected < indexed],
                                     np.arange(indexed, n, dtype=np.uint32)]).astype(np.uint32)
-        tot = totals.cpu().numpy()
         stats = QueryStats(groups_tested=int(tot[0]), keys_scanned=int(counts[2]),
                            f_scan=(counts[2] / n) if n else 1.0,
                            gate_cost_equiv=2.0 * float(tot[0]) / max(1, self.cfg.r))
         attention = None
         if counts[3]:
-            attended = selected if strict_threshold else retrieved
-            weights = None
-            if want_weights:
-                res = sparse_attention(self, np.zeros((0,), np.uint32), attended, q, req.effective_scale())
-                weights = res.weights if res is not None else None
-            attention = AttentionResult(selected_ids=attended, weights=weights, output=out)
+            attended = np.ascontiguousarray(selected if strict_threshold else retrieved, dtype=np.uint32)
+            weights = np.zeros((max(1, attended.size),), dtype=np.float32)
+            if attended.size:
+                check(self._ctx.lib.lv_attention_weights(self._ctx.h, 0, _ptr(attended), attended.size, _ptr(q),
+                                                         req.effective_scale(), float(part[0]), float(part[1]),
+                                                         LV_HOST, _ptr(weights), None), "attention weights")
+            attention = AttentionResult(selected_ids=attended, weights=weights[: attended.size], output=out)
         return CacheQueryResult(selected=selected, retrieved=retrieved, stats=stats, attention=attention)
+
+    def _lease(self):
+        torch = _torch()
+        words = self._ctx.bitmap_words
+        with self._pool_lock:
+            while self._pool:
+                bits, totals = self._pool.pop()
+                if bits.shape[1] == words:
+                    return bits, totals
+        return (torch.empty((1, words), dtype=torch.int32, device="cuda"),
+                torch.empty((4,), dtype=torch.int64, device="cuda"))
+
+    def _release(self, bits, totals):
+        with self._pool_lock:
+            self._pool.append((bits, totals))
 
 
 def brute_force_range(cache: LouverCache, q, tau: float, limit: Optional[int] = None) -> np.ndarray:
@@ -472,6 +497,22 @@ class LouverLayer:
         check(self._ctx.lib.lv_read_rows(self._ctx.h, slot, first, count, 1 if values else 0, _ptr(out)),
               "lv_read_rows")
         return out
+
+
+def query_layers_host(layers: Sequence["LouverLayer"], q: np.ndarray, tau: np.ndarray, out: np.ndarray, *,
+                      scale: float = 0.0, strict: bool = False, stream=None) -> np.ndarray:
+    """One decode step over L layers through the C ABI with HOST buffers (lv_query_layers):
+    q [L][batch][H_q][d], tau [L][batch][H_q], out [L][batch][H_q][d] float32, C-contiguous
+    (pinned for full speed). One copy in, L fused queries, one copy out, one sync."""
+    L = len(layers)
+    for a, shape in ((q, (L, layers[0].batch, layers[0].H_q, layers[0].d)), (tau, (L, layers[0].batch, layers[0].H_q)),
+                     (out, (L, layers[0].batch, layers[0].H_q, layers[0].d))):
+        if a.dtype != np.float32 or not a.flags.c_contiguous or a.shape != shape:
+            raise ValueError(f"query_layers_host: expected C-contiguous float32 {shape}")
+    hs = (C.c_void_p * L)(*[ly._ctx.h for ly in layers])
+    check(_capi.lib().lv_query_layers(hs, L, _ptr(q), _ptr(tau), float(scale), 1 if strict else 0, _ptr(out), None,
+                                      stream), "lv_query_layers")
+    return out
 
 
 def lse_merge(partials, out, stream=None) -> None:

@@ -6,6 +6,7 @@
 // brute force, strict toggle, flush-at-B), test_query.cpp:178-196 (attention
 // known answers / nullopt), and test_core.cpp error behaviour.
 // usage: test_host [--compile-only]
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -94,7 +95,44 @@ static void test_cache_fp32() {
                                                 req.effective_scale(), o.data(), nullptr, &ntok);
             EXPECT((rc == LVO_EMPTY) == !r.attention.has_value(), "q%d attention presence", qi);
             if (r.attention) EXPECT(rel_err(r.attention->output.data(), o.data(), d) <= 1e-4, "q%d attention", qi);
+            if (r.attention) {  // AttentionResult::weights aligned with the attended ids (query.cpp:359-365)
+                std::vector<float> w(att.size() ? att.size() : 1);
+                lvo_sparse_attention(K.data(), V.data(), n, d, nullptr, 0, att.data(), (int64_t)att.size(), q,
+                                     req.effective_scale(), o.data(), w.data(), &ntok);
+                EXPECT(r.attention->weights.size() == att.size(), "q%d weights size", qi);
+                double worst = 0.0;
+                for (size_t i = 0; i < att.size() && i < r.attention->weights.size(); ++i)
+                    worst = std::max(worst, std::fabs(double(r.attention->weights[i]) - w[i]) / (std::fabs(w[i]) + 1e-30));
+                EXPECT(worst <= 1e-4, "q%d weights rel err %g", qi, worst);
+            }
         }
+        // exact_check (query.cpp:22-31): every stored id as the candidate list, reversed
+        std::vector<KeyId> all(n);
+        for (int64_t j = 0; j < n; ++j) all[j] = (KeyId)(n - 1 - j);
+        EXPECT(exact_check(cache, all, {q, (size_t)d}, tau) == oracle_range(K, n, d, q, tau), "exact_check q%d", qi);
+        // query_ta's candidate set: a superset of the indexed selected keys, within [0, indexed)
+        const CandidateSet cs = query_ta(cache, req);
+        const auto sel_all = oracle_range(K, n, d, q, tau);
+        bool sup = true, inside = true;
+        for (KeyId id : sel_all)
+            if (id < cache.indexed_count() && !std::binary_search(cs.live_ids.begin(), cs.live_ids.end(), id)) sup = false;
+        for (KeyId id : cs.live_ids)
+            if (id >= cache.indexed_count()) inside = false;
+        EXPECT(sup && inside && std::is_sorted(cs.live_ids.begin(), cs.live_ids.end()), "query_ta candidates q%d", qi);
+        EXPECT(cs.stats.keys_scanned == (int64_t)cs.live_ids.size() && cs.stats.groups_tested > 0, "candidate stats");
+        // derive_subspace_thresholds: S = 1 gives tau itself; S = 4 thresholds are safe for every selected key
+        EXPECT(derive_subspace_thresholds(cache, {q, (size_t)d}, tau, 1)[0] == tau, "S=1 threshold");
+        const auto ts = derive_subspace_thresholds(cache, {q, (size_t)d}, tau, 4);
+        bool safe = ts.size() == 4;
+        for (KeyId id : sel_all) {
+            if (id >= cache.indexed_count()) continue;
+            for (int s = 0; s < 4 && safe; ++s) {
+                float part = 0.0f;  // the subspace's partial dot in the reference's order
+                for (int c = s * (d / 4); c < (s + 1) * (d / 4); ++c) part += q[c] * K[(size_t)id * d + c];
+                if (part < ts[s]) safe = false;
+            }
+        }
+        EXPECT(safe, "derive_subspace_thresholds safe q%d", qi);
         const auto bf = brute_force_range(cache, {q, (size_t)d}, tau, (size_t)n);
         EXPECT(bf == oracle_range(K, n, d, q, tau), "brute_force_range q%d", qi);
     }
@@ -109,6 +147,29 @@ static void test_cache_fp32() {
         for (float w : a->weights) s += w;
         EXPECT(std::fabs(s - 1.0) < 1e-5, "weights sum %f", s);
     }
+    // recall_at_k (query.cpp:374-383), store() (cache.hpp:49)
+    EXPECT(recall_at_k(std::vector<KeyId>{4, 1, 2, 3}, std::vector<KeyId>{9, 4, 2}) == 0.5, "recall_at_k");
+    bool threw_r = false;
+    try {
+        recall_at_k({}, std::vector<KeyId>{1});
+    } catch (const std::invalid_argument&) {
+        threw_r = true;
+    }
+    EXPECT(threw_r, "recall_at_k: k >= 1 required");
+    const KeyStore st = cache.store();
+    EXPECT(st.n() == (size_t)(n0 + extra) && std::memcmp(st.key_data(), K.data(), sizeof(float) * K.size()) == 0 &&
+               std::memcmp(st.value_data(), V.data(), sizeof(float) * V.size()) == 0,
+           "store() holds the stored rows");
+    EXPECT(cache.index().r == 16 && cache.index().indexed_count == cache.indexed_count(), "index() view");
+    bool threw_fs = false;
+    try {
+        QueryRequest rq;
+        rq.q.assign(Q.begin(), Q.begin() + d);
+        query_full_subspace(cache, rq, 4);
+    } catch (const std::invalid_argument&) {
+        threw_fs = true;
+    }
+    EXPECT(threw_fs, "query_full_subspace: tau_subspace required");
     // reference error behaviour
     bool threw = false;
     try {

@@ -87,6 +87,51 @@ def test_sparse_attention_vs_oracle(torch, oracle):  # test_query.cpp:198-223, a
     assert float(np.sum(got.weights, dtype=np.float64)) == pytest.approx(1.0, rel=1e-5)
 
 
+@pytest.mark.parametrize("strict", [False, True])
+def test_cache_query_weights_match_oracle(torch, oracle, strict):  # cache.cpp:67-68 -> query.cpp:356-369
+    k, v = synth.keys(4000, 64, 31), synth.keys(4000, 64, 32)
+    c = LouverCache.adopt(k[:3900], v[:3900], BuildConfig(S=4, r=16), 64)
+    for j in range(3900, 4000):
+        c.push_key(k[j], v[j])
+    q = synth.queries(1, 64, 31)[0]
+    tau = oracle.kth_score(k, q, 200)
+    res = c.query(QueryRequest(q=q, tau=float(tau)), FilterAlgo.Ta, strict)
+    att = res.attention
+    buf = [] if strict else list(range(c.indexed_count(), c.n()))
+    want = oracle.sparse_attention(k, v, buf, res.selected, q, np.float32(1 / 8))
+    assert list(att.selected_ids) == list(want[0])
+    assert att.weights.shape == (len(want[0]),)
+    np.testing.assert_allclose(att.weights, want[1], rtol=1e-4, atol=1e-9)
+    assert rel_err(att.output, want[2]) <= REL_TOL
+
+
+def test_query_layers_host_equals_device_queries(torch):
+    from paper_2605_06763_b200 import query_layers_host
+
+    L, H, G, d, n = 3, 2, 4, 128, 3000
+    layers, qs, ts = [], [], []
+    for l in range(L):
+        K = np.stack([synth.keys(n, d, 100 * l + h) for h in range(H)])[None]
+        V = np.stack([synth.keys(n, d, 100 * l + h + 50) for h in range(H)])[None]
+        Q = np.stack([synth.queries(G, d, 100 * l + h) for h in range(H)]).reshape(1, H * G, d)
+        ly = LouverLayer(d, H, G, 1, n, BuildConfig(S=1, r=16, grouping="contiguous", enclosing="aabb"))
+        ly.build(K, V)
+        layers.append(ly)
+        qs.append(Q.astype(np.float32))
+        ts.append(np.full((1, H * G), 40.0, np.float32))
+    q = np.ascontiguousarray(np.stack(qs))
+    t = np.ascontiguousarray(np.stack(ts))
+    out = np.zeros((L, 1, H * G, d), np.float32)
+    query_layers_host(layers, q, t, out)
+    for l in range(L):
+        want = torch.zeros((1, H * G, d), device="cuda")
+        layers[l].query_device(torch.from_numpy(qs[l]).cuda(), torch.from_numpy(ts[l]).cuda(), want)
+        torch.cuda.synchronize()
+        assert np.array_equal(out[l], want.cpu().numpy()), l
+    with pytest.raises(ValueError):
+        query_layers_host(layers, q[:, :, :4], t, out)
+
+
 def test_strict_toggle(torch):  # test_cache.cpp:123-144
     c = LouverCache(4, BuildConfig(S=2, r=2), 64)
     keys = np.array([[1, 1, 1, 1], [-1, -1, -1, -1], [2, 2, 2, 2]], np.float32)

@@ -525,7 +525,8 @@ inline std::optional<AttentionResult> sparse_attention(const LouverCache& cache,
 class LouverLayer {
   public:
     LouverLayer(int d, int n_kv_heads, int group_size, int batch, std::int64_t capacity, BuildConfig cfg,
-                std::size_t buffer_capacity, int dtype = LV_BF16) {
+                std::size_t buffer_capacity, int dtype = LV_BF16)
+        : d_(d), rows_(static_cast<std::int64_t>(batch) * n_kv_heads * group_size) {
         cfg.validate(d);
         lv_config c{};
         c.d = d;
@@ -571,9 +572,13 @@ class LouverLayer {
     }
     std::size_t workspace_bytes() const { return lv_query_workspace_bytes(ctx_.get()); }
     std::int64_t n() const { return lv_n(ctx_.get()); }
+    int dim() const { return d_; }
+    std::int64_t rows() const { return rows_; }  // batch x H_q query rows
     lv_ctx* handle() const { return ctx_.get(); }
 
   private:
+    int d_;
+    std::int64_t rows_;
     std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
 };
 

@@ -29,17 +29,20 @@ def insert_owner(world: int) -> int:
 
 
 def gather_partials(part, group=None):
-    """All-gather one rank's partials [rows][d+2] into [world][rows][d+2] (rank order)."""
-    import torch
+    """All-gather one rank's partials [rows][d+2] into [world][rows][d+2] (rank order).
+    NCCL gathers device tensors in place; with a CPU backend (gloo) device partials are
+    staged through host memory and the result is returned on the partials' device."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    out = part.new_empty((world,) + tuple(part.shape))
+    staged = part.is_cuda and dist.get_backend(group) != "nccl"
+    src = part.cpu() if staged else part
+    out = src.new_empty((world,) + tuple(src.shape))
     try:
-        dist.all_gather_into_tensor(out, part.contiguous(), group=group)
-    except (RuntimeError, NotImplementedError):  # backends without the fused collective
-        dist.all_gather(list(out.unbind(0)), part.contiguous(), group=group)
-    return out
+        dist.all_gather_into_tensor(out, src.contiguous(), group=group)
+    except (RuntimeError, NotImplementedError, ValueError):  # backends without the fused collective
+        dist.all_gather(list(out.unbind(0)), src.contiguous(), group=group)
+    return out.to(part.device, non_blocking=False) if staged else out
 
 
 class ShardedLayer:
@@ -56,7 +59,13 @@ class ShardedLayer:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
-    def query(self, q, tau, out, *, strict: bool = False, partial: Optional[object] = None):
+    def push_key(self, k, v, stream=None) -> None:
+        """One decode step's key/value per slot: appended by the tail shard only (it owns the
+        update buffer, so flush-at-B behaves as in one cache, cache.cpp:7-10)."""
+        if self.rank == insert_owner(self.world):
+            self.layer.push_key(k, v, stream=stream)
+
+    def query(self, q, tau, out, *, strict: bool = False, partial: Optional[object] = None, sel_bits=None):
         import torch
 
         from .louver import lse_merge
@@ -65,7 +74,7 @@ class ShardedLayer:
         d = out.shape[2]
         if partial is None:
             partial = torch.empty((out.shape[0], out.shape[1], d + 2), dtype=torch.float32, device=out.device)
-        self.layer.query_device(q, tau, None, strict=strict, partial=partial)
+        self.layer.query_device(q, tau, None, strict=strict, partial=partial, sel_bits=sel_bits)
         gathered = gather_partials(partial.view(rows, d + 2), self.group)
         lse_merge(gathered, out.view(rows, d))
         return out

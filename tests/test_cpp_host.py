@@ -29,3 +29,17 @@ def test_cpp_host_layer_matches_oracle():
     exe = _build()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
+
+
+def test_cpp_sharded_layer_compiles_and_links():  # include/louver_b200_nccl.hpp
+    _build()
+    exe = os.path.join(CPP, "test_sharded")
+    r = subprocess.run([exe, "--compile-only"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "nccl" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_sharded_layer_matches_unsharded():
+    _build()
+    r = subprocess.run([os.path.join(CPP, "test_sharded")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr

@@ -142,3 +142,92 @@ def test_two_shards_on_device_lse_merge(oracle, empty_shard):
         want = oracle.sparse_attention(K[0, hq // G], V[0, hq // G], [], ids, Q[0, hq], np.float32(1 / math.sqrt(d)))
         assert want is not None
         assert np.linalg.norm(o[hq] - want[2]) <= 1e-4 * np.linalg.norm(want[2]), hq
+
+
+# ---------------------------------------------------------------------------------------------
+# ShardedLayer end to end: two processes on one GPU (gloo, partials staged through host
+# memory), the product kernels on each shard, decode-step inserts into the tail shard across
+# a flush, against the unsharded oracle cache (LouverCache with the same prompt and pushes).
+
+_SH = dict(d=128, H=2, G=4, n0=4000, extra=96, B=64)
+
+
+def _sharded_inputs():
+    import torch
+
+    c = _SH
+    n = c["n0"] + c["extra"]
+    K = np.stack([synth.keys(n, c["d"], 900 + h) for h in range(c["H"])])  # [H][n][d]
+    V = np.stack([synth.keys(n, c["d"], 950 + h) for h in range(c["H"])])
+    Q = np.stack([synth.queries(c["G"], c["d"], 900 + h) for h in range(c["H"])]).reshape(c["H"] * c["G"], c["d"])
+    K = torch.from_numpy(K).to(torch.bfloat16).float().numpy()
+    V = torch.from_numpy(V).to(torch.bfloat16).float().numpy()
+    return K, V, Q.astype(np.float32)
+
+
+def _sharded_rank(rank, world, port, tau, out_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_06763_b200 import BuildConfig, LouverLayer, ShardedLayer
+
+    c = _SH
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    K, V, Q = _sharded_inputs()
+    first, count = shard_range(c["n0"], world, rank)
+    layer = LouverLayer(c["d"], c["H"], c["G"], 1, count + c["extra"] + 16,
+                        BuildConfig(S=1, r=16, grouping="contiguous", enclosing="aabb"), buffer_capacity=c["B"])
+    layer.build(np.ascontiguousarray(K[None, :, first:first + count]), np.ascontiguousarray(V[None, :, first:first + count]))
+    sh = ShardedLayer(layer)
+    for j in range(c["n0"], c["n0"] + c["extra"]):
+        sh.push_key(torch.from_numpy(np.ascontiguousarray(K[None, :, j])).cuda(),
+                    torch.from_numpy(np.ascontiguousarray(V[None, :, j])).cuda())
+    q = torch.from_numpy(Q[None]).cuda()
+    t = torch.from_numpy(np.asarray(tau, np.float32)[None]).cuda()
+    out = torch.zeros((1, c["H"] * c["G"], c["d"]), device="cuda")
+    bits = torch.zeros((c["H"] * c["G"], layer.bitmap_words), dtype=torch.int32, device="cuda")
+    sh.query(q, t, out, sel_bits=bits)
+    torch.cuda.synchronize()
+    ids = [np.asarray(x, np.int64) + first for x in layer.ids_from_bits(bits)]
+    allids = [None] * world
+    dist.all_gather_object(allids, ids)
+    if rank == 0:
+        np.savez(out_path, out=out.cpu().numpy()[0], flushes=layer.flush_count,
+                 **{f"ids{r}_{h}": allids[r][h] for r in range(world) for h in range(len(ids))})
+    else:
+        np.save(out_path + ".tail.npy", np.array([layer.flush_count, layer.indexed_count, layer.n]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_layer_two_processes_with_tail_inserts(oracle):
+    import torch.multiprocessing as mp
+
+    c = _SH
+    K, V, Q = _sharded_inputs()
+    n = c["n0"] + c["extra"]
+    rq = c["H"] * c["G"]
+    # the global ceil(0.05 n)-th score per q head over the whole (sharded) context
+    tau = [float(np.sort(oracle.scores(K[hq // c["G"]], Q[hq]))[::-1][int(math.ceil(0.05 * n)) - 1]) for hq in range(rq)]
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "sh.npz")
+        mp.start_processes(_sharded_rank, args=(2, _free_port(), tau, path), nprocs=2, join=True, start_method="spawn")
+        got = np.load(path)
+        tail = np.load(path + ".tail.npy")
+        out = got["out"]
+        ids = [np.sort(np.concatenate([got[f"ids{r}_{h}"] for r in range(2)])) for h in range(rq)]
+    # the tail shard flushed once (96 pushes, B = 64) and holds 32 buffer keys
+    assert tail[0] == c["extra"] // c["B"] and tail[2] - tail[1] == c["extra"] % c["B"]
+    for h in range(c["H"]):
+        cache = oracle.Cache(c["d"], oracle.cfg(1, 16, "contiguous", "aabb"), c["B"], keys=K[h, :c["n0"]],
+                             values=V[h, :c["n0"]])
+        for j in range(c["n0"], n):
+            cache.push_key(K[h, j], V[h, j])
+        for g in range(c["G"]):
+            hq = h * c["G"] + g
+            r = cache.query(Q[hq], tau[hq])
+            sel, o_want = r["selected"], r["output"]
+            assert np.array_equal(ids[hq], np.asarray(sel, np.int64)), hq
+            assert np.linalg.norm(out[hq] - o_want) <= 1e-4 * np.linalg.norm(o_want), hq

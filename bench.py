@@ -66,8 +66,10 @@ def layer_seeds(layer: int, rank: int, b: int, h: int, H_kv: int) -> int:
     return 1_000_003 * (layer + 1) + 10_007 * rank + 1000 * (b * H_kv + h) + 17
 
 
-def gen_layer(cfg, layer, rank, threads):
-    """K, V [batch][H_kv][n][d] fp32 (reference key law), Q [batch][H_q][d]."""
+def gen_layer(cfg, layer, rank, threads, qsteps=1):
+    """K, V [batch][H_kv][n][d] fp32 (reference key law), Q [batch][H_q][d]; with qsteps > 1,
+    Q is [qsteps][batch][H_q][d]: consecutive decode queries of the same stream
+    (gen_synthetic_queries rows, io.cpp:186-202; step 0 = the single-query rows)."""
     from paper_2605_06763_b200 import synth
 
     B, H, G, d, n = cfg["batch"], cfg["H_kv"], cfg["G"], cfg["d"], cfg["n"]
@@ -75,9 +77,11 @@ def gen_layer(cfg, layer, rank, threads):
     K = synth.keys_multi(n, d, seeds, threads).reshape(B, H, n, d)
     V = synth.keys_multi(n, d, seeds + np.uint64(1), threads).reshape(B, H, n, d)
     # queries follow the layer's key stream direction (independent of the rank's shard)
-    Q = np.stack([np.stack([synth.queries(G, d, int(layer_seeds(layer, 0, b, h, H))) for h in range(H)])
-                  for b in range(B)]).reshape(B, H * G, d)
-    return K, V, Q
+    R = max(1, qsteps)
+    Q = np.stack([np.stack([synth.queries(G * R, d, int(layer_seeds(layer, 0, b, h, H))).reshape(R, G, d)
+                            for h in range(H)], axis=1) for b in range(B)], axis=1)  # [R][B][H][G][d]
+    Q = Q.reshape(R, B, H * G, d)
+    return (K, V, Q[0]) if qsteps <= 1 else (K, V, Q)
 
 
 def top_scores(torch, K, Q, G, k):
@@ -321,6 +325,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-dense-lib", action="store_true", help="skip the library (torch SDPA) dense decode")
+    ap.add_argument("--qsteps", type=int, default=4,
+                    help="distinct consecutive decode queries per layer, cycled through the timed steps")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -352,20 +358,27 @@ def main():
     build_cfg = BuildConfig(S=1, r=CELL, grouping="contiguous", enclosing="aabb")
 
     layers, qs, taus, outs, kts, vts = [], [], [], [], [], []
+    qsets, tsets = [], []  # [L][R]: the decode stream's consecutive queries and their tau
+    R = max(1, args.qsteps)
     first = None
     t0 = time.perf_counter()
     for l in range(L):
-        K, V, Q = gen_layer(cfg, l, rank, threads)
+        K, V, QR = gen_layer(cfg, l, rank, threads, qsteps=R if R > 1 else 1)
+        QR = QR if R > 1 else QR[None]
+        Q = QR[0]
         layer = LouverLayer(d, H, G, B, n, build_cfg, buffer_capacity=128, dtype=cfg["dtype"])
         layer.build(K, V)
-        tau = taus_device(torch, K, Q, G, SELECTIVITY, world, dist if world > 1 else None)
+        tr = [taus_device(torch, K, QR[i], G, SELECTIVITY, world, dist if world > 1 else None) for i in range(R)]
+        tau = tr[0]
+        qsets.append([torch.from_numpy(QR[i]).cuda() for i in range(R)])
+        tsets.append([torch.from_numpy(tr[i]).cuda() for i in range(R)])
         layers.append(layer)
         if not args.no_dense_lib:  # [B][H][n][d] copies (config dtype) for the library dense decode (SDPA)
             tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
             kts.append(torch.from_numpy(K).to("cuda", tdt))
             vts.append(torch.from_numpy(V).to("cuda", tdt))
-        qs.append(torch.from_numpy(Q).cuda())
-        taus.append(torch.from_numpy(tau).cuda())
+        qs.append(qsets[-1][0])
+        taus.append(tsets[-1][0])
         outs.append(torch.zeros((B, H_q, d), dtype=torch.float32, device="cuda"))
         if l == 0:
             first = (K, V, Q, tau)
@@ -373,13 +386,14 @@ def main():
     setup_s = time.perf_counter() - t0
     log(f"[rank {rank}] setup {setup_s:.1f}s: {L} layers x {B}x{H} slots x {n} keys ({cfg['dtype']})")
 
-    # ---- per-layer work accounting (outside the timed region)
-    totals = torch.zeros((L, 4), dtype=torch.int64, device="cuda")
-    counts = torch.zeros((L, B, H_q, 4), dtype=torch.int32, device="cuda")
-    for l in range(L):
-        layers[l].query_device(qs[l], taus[l], outs[l], totals=totals[l], counts=counts[l])
+    # ---- per-layer work accounting (outside the timed region), averaged over the R queries
+    totals = torch.zeros((R, L, 4), dtype=torch.int64, device="cuda")
+    counts = torch.zeros((R, L, B, H_q, 4), dtype=torch.int32, device="cuda")
+    for i in range(R):
+        for l in range(L):
+            layers[l].query_device(qsets[l][i], tsets[l][i], outs[l], totals=totals[i, l], counts=counts[i, l])
     torch.cuda.synchronize()
-    tot = totals.cpu().numpy().astype(np.float64)
+    tot = totals.cpu().numpy().astype(np.float64).reshape(R * L, 4)
     cnt = counts.cpu().numpy().astype(np.float64)
     # partials: [slots][splits][G][d+2] fp32 written by every CTA, read by the merge
     slots = B * H
@@ -401,29 +415,36 @@ def main():
         parts = [torch.zeros((B, H_q, d + 2), dtype=torch.float32, device="cuda") for _ in range(L)]
         gathered = [torch.zeros((world, B * H_q, d + 2), dtype=torch.float32, device="cuda") for _ in range(L)]
 
-    def step():
+    def step(i=0):  # decode step i of the stream: query i % R of every layer
         for l in range(L):
+            q, t = qsets[l][i % R], tsets[l][i % R]
             if world > 1:
-                layers[l].query_device(qs[l], taus[l], None, partial=parts[l])
+                layers[l].query_device(q, t, None, partial=parts[l])
                 dist.all_gather_into_tensor(gathered[l], parts[l].view(B * H_q, d + 2))
                 lse_merge(gathered[l], outs[l].view(B * H_q, d))
             else:
-                layers[l].query_device(qs[l], taus[l], outs[l])
+                layers[l].query_device(q, t, outs[l])
+
+    def steps_block():  # R consecutive decode steps
+        for i in range(R):
+            step(i)
 
     graph = None
     if world == 1 and not args.no_graph:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            step()  # warm the lazy attribute setup outside capture
+            steps_block()  # warm the lazy attribute setup outside capture
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
-    run = graph.replay if graph is not None else step
+            steps_block()
+    # one run = R decode steps; the timed region is ceil(steps / R) runs
+    run = graph.replay if graph is not None else steps_block
+    args.steps = -(-args.steps // R) * R
 
-    for _ in range(args.warmup):
+    for _ in range(-(-args.warmup // R)):
         run()
     torch.cuda.synchronize()
     if world > 1:
@@ -432,7 +453,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         ev0.record()
-        for _ in range(args.steps):
+        for _ in range(args.steps // R):
             run()
         ev1.record()
         torch.cuda.synchronize()
@@ -628,6 +649,8 @@ def main():
             "workload": cfg["workload"] + (f"; sequence-sharded {n} keys/GPU, context {n * world}" if world > 1 else ""),
             "batch": B, "H_q": H_q, "H_kv": H, "d": d, "n_per_gpu": n, "context": n * world, "layers": L,
             "cell_keys": CELL, "selectivity": SELECTIVITY, "tau": "fixed, ceil(0.05 n)-th largest score",
+            "queries": (f"{R} consecutive decode queries per layer (rows of the stream's "
+                        f"gen_synthetic_queries), step i uses query i % {R}, each with its own tau"),
             "l2": f"inputs larger than L2: {L} layers x {slots * n * d * e * 2 / 2**20:.0f} MiB KV; "
                   f"{alg_bytes * L / 1e6:.0f} MB touched per step",
             "parallelism": f"seq-shard{world}" if world > 1 else "single GPU",

@@ -88,6 +88,14 @@ typedef struct {
     uint64_t rng_seed;
     int64_t buffer_capacity; /* B >= 1: keys [indexed_count, n) form the dense-scanned buffer */
     int64_t capacity;        /* max keys per sequence held in the HBM arena */
+    /* 1: also build the reference's grouped index on the device — S subspaces, the
+     * configured GroupingStrategy (PCA tree included) and EnclosureKind, packed gate
+     * arrays and member lists, bit-exact with index.cpp — at lv_build and at every flush.
+     * It serves lv_group_candidates / lv_group_thresholds (the reference's candidate sets
+     * and QueryStats) and lv_save_index (the reference's snapshot of that index). The
+     * fused query does not use it (its final sets do not depend on the grouping).
+     * Memory: about the fp32 key arena again. 0: off. */
+    int group_index;
 } lv_config;
 
 typedef struct {
@@ -110,6 +118,16 @@ typedef struct {
                             query_ta / query_full_subspace (query.hpp:48-58) — every INDEXED key
                             of a cell whose bound reaches any q head's threshold (fp32 caches) */
 } lv_query_args;
+
+/* QueryStats (query.hpp:24-32) of a candidate filter on the grouped index. */
+typedef struct {
+    int64_t groups_tested;  /* sum over subspaces */
+    int64_t keys_scanned;   /* |live_ids| */
+    double f_scan;          /* keys_scanned / indexed_count */
+    double gate_cost_equiv; /* g * groups_tested / r, g = 2 for AABB, 1 for balls */
+    int32_t ta_stop_depth;  /* -1: the TA scan did not halt early (or FullSubspace) */
+    double ta_stop_upper;   /* U(d*) when it halted */
+} lv_group_stats;
 
 const char* lv_last_error(void);
 
@@ -235,6 +253,26 @@ int lv_dense_decode(lv_ctx* ctx, const float* q, float scale, int where, float* 
 
 /* Log-sum-exp merge of P shard partials [P][rows][d+2] (m, l, o unnormalised)
  * into out[rows][d] (device pointers). Empty shards carry m = -inf, l = 0. */
+/* Grouped index (lv_config.group_index = 1), for one slot (sequence x kv head).
+ * lv_group_candidates: the candidate set of query_full_subspace (algo
+ * LV_ALGO_FULL_SUBSPACE; tau_subspace[S] required, host) or query_ta (LV_ALGO_TA)
+ * (query.cpp:82-303) for the host query q[d] — live_bits: optional DEVICE bitmap of
+ * lv_bitmap_words() words over the indexed keys; live_ids: optional HOST array of `cap`
+ * ids (ascending), *nlive its length; stats: optional HOST. Synchronises `stream`.
+ * lv_group_thresholds: derive_subspace_thresholds (query.cpp:305-336), out[S] host.
+ * lv_group_count: groups per subspace (K, the same for every slot and subspace).
+ * lv_group_export: HOST copies of subspace s of a slot — assignments[indexed],
+ * member offsets[K + 1], member ids[indexed] (ascending within each group), gate arrays
+ * coordinate-major [w][K] (a: centers for balls, lo for AABB; b: hi for AABB), radii[K]
+ * and norm_bound; any pointer may be NULL. */
+int lv_group_candidates(lv_ctx* ctx, int slot, const float* q, float tau, const float* tau_subspace, int algo,
+                        uint32_t* live_bits, uint32_t* live_ids, int64_t cap, int64_t* nlive,
+                        lv_group_stats* stats, void* stream);
+int lv_group_thresholds(lv_ctx* ctx, int slot, const float* q, float tau, float* out, void* stream);
+int64_t lv_group_count(const lv_ctx* ctx);
+int lv_group_export(const lv_ctx* ctx, int slot, int s, uint32_t* assignments, uint32_t* member_offsets,
+                    uint32_t* member_ids, float* a, float* b, float* radii, double* norm_bound);
+
 int lv_lse_merge(const float* partials, int P, int64_t rows, int d, float* out, void* stream);
 
 /* --- Threshold oracle (threshold.hpp:9-53, threshold.cpp:40-103) --------------
@@ -310,14 +348,20 @@ int lv_step_advance(int64_t* step, void* stream);
  * std::runtime_error (LV_ERUNTIME): bad magic, truncation, trailing bytes. */
 int lv_save_dataset(const char* path, const float* data, int64_t n, int d);
 int lv_load_dataset(const char* path, float* out, int64_t cap_rows, int64_t* n, int* d);
-/* "LVIX" index snapshot of slot `slot`: the device cells written as the
+/* "LVIX" index snapshot of slot `slot` (io.cpp:236-268). With the grouped index
+ * (lv_config.group_index) it is that index, byte for byte the reference's save_index
+ * of the same BuildConfig and keys; without it, the device cells written in the
  * reference's format (S = 1, contiguous groups of r keys, exact fp32 AABBs of the
  * stored keys, indexed_count = lv_indexed_count). */
 int lv_save_index(const lv_ctx* ctx, int slot, const char* path);
 /* Reads any reference LVIX file (every grouping / enclosure / S), checks it
  * against the cache (dimension, indexed_count <= n, groups partitioning the
  * indexed keys consistently with the assignments, no trailing bytes) and adopts
- * its indexed_count: keys past it become the buffer. */
+ * its indexed_count: keys past it become the buffer. With the grouped index (one
+ * slot, the snapshot's BuildConfig equal to the cache's) the snapshot's groups,
+ * enclosures and members become the grouped index, gate arrays and norm bounds
+ * derived as load_index does (io.cpp:309); otherwise the grouped index is rebuilt over
+ * [0, indexed_count) with the cache's BuildConfig. */
 int lv_load_index(lv_ctx* ctx, const char* path, int64_t* indexed_count, void* stream);
 
 /* Host-side synthetic streams with the reference laws (io.cpp:89-206);

@@ -941,6 +941,58 @@ int64_t lvo_cache_group_members(const lvo_cache* c, int s, int64_t g, uint32_t* 
     return cnt;
 }
 
+int lvo_cache_candidates(const lvo_cache* c, const float* q, float tau, const float* tau_s, int algo,
+                         uint32_t* ids, int64_t cap, int64_t* n, lvo_stats* stats) {
+    return guarded([&] {
+        if (!c->has_index) throw std::invalid_argument("candidates: no index");
+        Cands cand;
+        if (algo == 0) {
+            if (!tau_s) throw std::invalid_argument("query_full_subspace: tau_subspace required");
+            cand = full_subspace(c->idx, q, std::vector<float>(tau_s, tau_s + c->idx.subs.size()));
+        } else {
+            cand = ta_scan(c->idx, q, tau);
+        }
+        copy_ids(cand.live, ids, cap, n);
+        if (stats) {
+            stats->groups_tested = cand.st.groups;
+            stats->keys_scanned = cand.st.scanned;
+            stats->f_scan = cand.st.f_scan;
+            stats->gate_cost_equiv = cand.st.gate_cost;
+            stats->ta_stop_depth = cand.st.stop_depth;
+            stats->ta_stop_upper = cand.st.stop_upper;
+        }
+        return LVO_OK;
+    });
+}
+
+int lvo_cache_thresholds(const lvo_cache* c, const float* q, float tau, float* out) {
+    return guarded([&] {
+        if (!c->has_index) throw std::invalid_argument("thresholds: no index");
+        const auto t = subspace_taus(c->idx, q, tau);
+        std::memcpy(out, t.data(), sizeof(float) * t.size());
+        return LVO_OK;
+    });
+}
+
+int lvo_cache_subspace(const lvo_cache* c, int s, uint32_t* assign, uint32_t* moff, uint32_t* mids, float* a,
+                       float* b, float* radii, double* norm_bound) {
+    return guarded([&] {
+        if (!c->has_index || s < 0 || s >= (int)c->idx.subs.size()) throw std::out_of_range("subspace");
+        const Sub& sb = c->idx.subs[s];
+        const std::size_t K = sb.groups();
+        if (assign) std::memcpy(assign, sb.assign.data(), sizeof(uint32_t) * sb.assign.size());
+        if (moff) std::memcpy(moff, sb.moff.data(), sizeof(uint32_t) * sb.moff.size());
+        if (mids) std::memcpy(mids, sb.mids.data(), sizeof(uint32_t) * sb.mids.size());
+        const bool box = c->cfg.enclosure == kAabb;
+        const auto& A = box ? sb.glo : sb.gc;
+        for (std::size_t i = 0; a && i < A.size(); ++i) std::memcpy(a + i * K, A[i].data(), sizeof(float) * K);
+        for (std::size_t i = 0; b && box && i < sb.ghi.size(); ++i) std::memcpy(b + i * K, sb.ghi[i].data(), sizeof(float) * K);
+        if (radii && !box) std::memcpy(radii, sb.grad.data(), sizeof(float) * K);
+        if (norm_bound) *norm_bound = sb.norm_bound;
+        return LVO_OK;
+    });
+}
+
 // cache.cpp:30-70
 int lvo_cache_query(const lvo_cache* c, const float* q, float tau, float scale, int algo,
                     int strict, uint32_t* selected, int64_t* nsel, uint32_t* retrieved,

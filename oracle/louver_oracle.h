@@ -104,6 +104,18 @@ int lvo_cache_query(const lvo_cache* c, const float* q, float tau, float scale, 
                     int64_t* nret, int64_t cap, float* attn_out, int* has_attn,
                     lvo_stats* stats);
 
+/* The cache's index directly (cache.hpp:49-50 index()): the candidate set of
+ * query_full_subspace (algo 0; tau_s[S] required) or query_ta (algo 1) with its stats
+ * (query.cpp:82-303), derive_subspace_thresholds (query.cpp:305-336, out[S]), and one
+ * subspace's arrays (index.hpp:29-52): assignments[indexed], member offsets[K + 1],
+ * member ids[indexed], gate arrays [w][K] (a: centers or lo, b: hi), radii[K], norm_bound.
+ * Any output pointer may be NULL. */
+int lvo_cache_candidates(const lvo_cache* c, const float* q, float tau, const float* tau_s, int algo,
+                         uint32_t* ids, int64_t cap, int64_t* n, lvo_stats* stats);
+int lvo_cache_thresholds(const lvo_cache* c, const float* q, float tau, float* out);
+int lvo_cache_subspace(const lvo_cache* c, int s, uint32_t* assign, uint32_t* moff, uint32_t* mids,
+                       float* a, float* b, float* radii, double* norm_bound);
+
 /* --- Index-level entry points used by tests ------------------------------- */
 /* index.cpp:15-68; points [m][w]; out assignments[m] */
 int lvo_balanced_pca_tree(const float* points, int64_t m, int w, int r, uint32_t* out);

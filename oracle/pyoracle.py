@@ -63,6 +63,10 @@ _SIGS = {
     "lvo_cache_group_members": (C.c_int64, [_P, C.c_int, C.c_int64, _P, C.c_int64]),
     "lvo_cache_query": (C.c_int, [_P, _P, C.c_float, C.c_float, C.c_int, C.c_int, _P, _I64P, _P, _I64P,
                                   C.c_int64, _P, C.POINTER(C.c_int), C.POINTER(lvo_stats)]),
+    "lvo_cache_candidates": (C.c_int, [_P, _P, C.c_float, _P, C.c_int, _P, C.c_int64, _I64P,
+                                       C.POINTER(lvo_stats)]),
+    "lvo_cache_thresholds": (C.c_int, [_P, _P, C.c_float, _P]),
+    "lvo_cache_subspace": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, C.POINTER(C.c_double)]),
     "lvo_balanced_pca_tree": (C.c_int, [_P, C.c_int64, C.c_int, C.c_int, _P]),
     "lvo_assign_groups": (C.c_int, [_P, C.c_int64, C.c_int, C.POINTER(lvo_build_config), C.c_int,
                                     C.c_uint32, _P]),
@@ -314,6 +318,45 @@ class Cache:
         out = np.zeros((4096,), np.uint32)
         cnt = lib().lvo_cache_group_members(self.h, s, g, out.ctypes.data, out.size)
         return out[:cnt].copy()
+
+    def candidates(self, q, tau, algo: int = 1, tau_s=None):
+        """query_full_subspace (algo 0, tau_s required) / query_ta (algo 1) on the cache's
+        index: (live ids, stats dict)."""
+        q = _f32(q).reshape(-1)
+        n = max(1, self.indexed_count())
+        ids = np.empty((n,), np.uint32)
+        cnt = C.c_int64()
+        st = lvo_stats()
+        ts = None if tau_s is None else _f32(tau_s)
+        _check(lib().lvo_cache_candidates(self.h, q.ctypes.data, float(np.float32(tau)),
+                                          None if ts is None else ts.ctypes.data, algo, ids.ctypes.data, n,
+                                          C.byref(cnt), C.byref(st)))
+        stats = dict(groups_tested=st.groups_tested, keys_scanned=st.keys_scanned, f_scan=st.f_scan,
+                     gate_cost_equiv=st.gate_cost_equiv, ta_stop_depth=st.ta_stop_depth,
+                     ta_stop_upper=st.ta_stop_upper)
+        return ids[: cnt.value].copy(), stats
+
+    def thresholds(self, q, tau, S: int) -> np.ndarray:
+        q = _f32(q).reshape(-1)
+        out = np.zeros((S,), np.float32)
+        _check(lib().lvo_cache_thresholds(self.h, q.ctypes.data, float(np.float32(tau)), out.ctypes.data))
+        return out
+
+    def subspace(self, s: int, w: int, enclosure: str):
+        """(assignments, member offsets, member ids, a [w][K], b [w][K] | None, radii | None, norm_bound)"""
+        n, K = self.indexed_count(), self.groups(s)
+        asg = np.zeros((max(n, 1),), np.uint32)
+        off = np.zeros((K + 1,), np.uint32)
+        mem = np.zeros((max(n, 1),), np.uint32)
+        a = np.zeros((w, max(K, 1)), np.float32)
+        b = np.zeros((w, max(K, 1)), np.float32)
+        rad = np.zeros((max(K, 1),), np.float32)
+        nb = C.c_double()
+        _check(lib().lvo_cache_subspace(self.h, s, asg.ctypes.data, off.ctypes.data, mem.ctypes.data,
+                                        a.ctypes.data, b.ctypes.data, rad.ctypes.data, C.byref(nb)))
+        box = enclosure == "aabb"
+        return (asg[:n], off, mem[:n], a[:, :K].copy(), b[:, :K].copy() if box else None,
+                None if box else rad[:K].copy(), nb.value)
 
     def query(self, q, tau, algo: int = 1, strict: bool = False, scale: float = 0.0):
         """Returns dict(selected, retrieved, output|None, stats)."""

@@ -242,6 +242,67 @@ int lvo_cache_query(const lvo_cache* c, const float* q, float tau, float scale, 
     });
 }
 
+int lvo_cache_candidates(const lvo_cache* c, const float* q, float tau, const float* tau_s, int algo,
+                         uint32_t* ids, int64_t cap, int64_t* n, lvo_stats* stats) {
+    return guarded([&] {
+        const auto& idx = c->c->index();
+        const int d = c->c->store().dim();
+        QueryRequest req;
+        req.q = vec_of(q, d);
+        req.tau = tau;
+        if (tau_s) req.tau_subspace = std::vector<Scalar>(tau_s, tau_s + idx.layout.S);
+        const CandidateSet cs = algo == 0 ? query_full_subspace(idx, c->c->store(), req)
+                                          : query_ta(idx, c->c->store(), req);
+        copy_ids(cs.live_ids, ids, cap, n);
+        if (stats) {
+            stats->groups_tested = cs.stats.groups_tested;
+            stats->keys_scanned = cs.stats.keys_scanned;
+            stats->f_scan = cs.stats.f_scan;
+            stats->gate_cost_equiv = cs.stats.gate_cost_equiv;
+            stats->ta_stop_depth = cs.stats.ta_stop_depth ? *cs.stats.ta_stop_depth : -1;
+            stats->ta_stop_upper = cs.stats.ta_stop_upper ? *cs.stats.ta_stop_upper : 0.0;
+        }
+        return LVO_OK;
+    });
+}
+
+int lvo_cache_thresholds(const lvo_cache* c, const float* q, float tau, float* out) {
+    return guarded([&] {
+        const int d = c->c->store().dim();
+        const auto t = derive_subspace_thresholds(c->c->index(), vec_of(q, d), tau);
+        std::memcpy(out, t.data(), sizeof(float) * t.size());
+        return LVO_OK;
+    });
+}
+
+int lvo_cache_subspace(const lvo_cache* c, int s, uint32_t* assign, uint32_t* moff, uint32_t* mids, float* a,
+                       float* b, float* radii, double* norm_bound) {
+    return guarded([&] {
+        const auto& idx = c->c->index();
+        if (s < 0 || s >= (int)idx.per_subspace.size()) throw std::out_of_range("subspace");
+        const auto& sb = idx.per_subspace[s];
+        const std::size_t K = sb.groups.size();
+        if (assign) std::memcpy(assign, sb.assignments.data(), sizeof(uint32_t) * sb.assignments.size());
+        if (moff) std::memcpy(moff, sb.member_offsets.data(), sizeof(uint32_t) * sb.member_offsets.size());
+        if (mids) std::memcpy(mids, sb.member_ids.data(), sizeof(uint32_t) * sb.member_ids.size());
+        const bool box = idx.config.enclosing == EnclosureKind::Aabb;
+        const auto& A = box ? sb.gate_lo : sb.gate_centers;
+        for (std::size_t i = 0; a && i < A.size(); ++i) std::memcpy(a + i * K, A[i].data(), sizeof(float) * K);
+        for (std::size_t i = 0; b && box && i < sb.gate_hi.size(); ++i)
+            std::memcpy(b + i * K, sb.gate_hi[i].data(), sizeof(float) * K);
+        if (radii && !box) std::memcpy(radii, sb.gate_radii.data(), sizeof(float) * K);
+        if (norm_bound) *norm_bound = sb.norm_bound;
+        return LVO_OK;
+    });
+}
+
+int lvr_cache_save_index(const lvo_cache* c, const char* path) {
+    return guarded([&] {
+        save_index(path, c->c->index());
+        return LVO_OK;
+    });
+}
+
 int lvo_balanced_pca_tree(const float* points, int64_t m, int w, int r, uint32_t* out) {
     return guarded([&] {
         const Matrix p = rows_of(points, m, w);

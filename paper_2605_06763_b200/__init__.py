@@ -22,20 +22,26 @@ from .louver import (  # noqa: F401
     AttentionResult,
     BuildConfig,
     CacheQueryResult,
+    CandidateSet,
     FilterAlgo,
     LouverCache,
     LouverLayer,
     QueryRequest,
     QueryStats,
     brute_force_range,
+    derive_subspace_thresholds,
     lse_merge,
+    query_full_subspace,
+    query_ta,
     query_layers_host,
     sparse_attention,
+    SubspaceIndex,
 )
 
 __all__ = [
     "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
-    "QueryRequest", "QueryStats", "brute_force_range", "lse_merge", "query_layers_host", "sparse_attention", "LouverError",
+    "QueryRequest", "QueryStats", "CandidateSet", "SubspaceIndex", "query_ta", "query_full_subspace",
+    "derive_subspace_thresholds", "brute_force_range", "lse_merge", "query_layers_host", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
     "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim", "GraphDecodeReport", "run_decode_graph",

@@ -34,6 +34,18 @@ class lv_config(C.Structure):
         ("rng_seed", C.c_uint64),
         ("buffer_capacity", C.c_int64),
         ("capacity", C.c_int64),
+        ("group_index", C.c_int),
+    ]
+
+
+class lv_group_stats(C.Structure):
+    _fields_ = [
+        ("groups_tested", C.c_int64),
+        ("keys_scanned", C.c_int64),
+        ("f_scan", C.c_double),
+        ("gate_cost_equiv", C.c_double),
+        ("ta_stop_depth", C.c_int32),
+        ("ta_stop_upper", C.c_double),
     ]
 
 
@@ -131,6 +143,11 @@ _SIGS = {
     "lv_step_store": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
     "lv_step_reservoir": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int, C.c_int64, _P]),
     "lv_step_advance": (C.c_int, [_P, _P]),
+    "lv_group_candidates": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_int, _P, _P, C.c_int64,
+                                      C.POINTER(C.c_int64), C.POINTER(lv_group_stats), _P]),
+    "lv_group_thresholds": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, _P]),
+    "lv_group_count": (C.c_int64, [_P]),
+    "lv_group_export": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, C.POINTER(C.c_double)]),
     "lv_estimate_tau": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P]),
 }
 

@@ -17,6 +17,7 @@
 #include "louver_b200.h"
 #include "louver_threshold.cuh"
 #include "louver_dispatch.h"
+#include "louver_groups.h"
 #include "louver_launch.h"
 #include "louver_v9.cuh"
 
@@ -87,6 +88,7 @@ struct lv_ctx {
     int l2pf = 0;                // experiment knob (LV_L2PF)
     int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
+    lvg::GroupIndex* gi = nullptr;  // the reference's grouped index (cfg.group_index)
     std::mutex writer;
 };
 
@@ -138,6 +140,8 @@ int validate(const lv_config* c) {
     if (c->S < 1) return fail(LV_EINVAL, "BuildConfig: S >= 1 required");
     if (c->r < 1) return fail(LV_EINVAL, "BuildConfig: r >= 1 required");
     if (c->S > c->d) return fail(LV_EINVAL, "BuildConfig: S <= d required");
+    if (c->group_index != 0 && c->group_index != 1) return fail(LV_EINVAL, "lv_create: group_index must be 0 or 1");
+    if (c->group_index && c->S > 64) return fail(LV_EINVAL, "lv_create: the grouped index supports S <= 64");
     if (c->grouping < 0 || c->grouping > 3 || c->enclosure < 0 || c->enclosure > 2)
         return fail(LV_EINVAL, "BuildConfig: unknown grouping or enclosure");
     if (c->buffer_capacity < 1)
@@ -241,6 +245,15 @@ int convert_into(lv_ctx* c, const void* src_dev, int src_dtype, void* arena, lon
                   : launch_convert<float, float>(c, src_dev, arena, n, first, st);
     if (!bf) return fail(LV_EINVAL, "bf16 source needs a bf16 cache");
     return launch_convert<__nv_bfloat16, __nv_bfloat16>(c, src_dev, arena, n, first, st);
+}
+
+lvg::ArenaView arena_view(const lv_ctx* c) {
+    lvg::ArenaView a;
+    a.K = c->K;
+    a.bf16 = c->cfg.dtype == LV_BF16;
+    a.DP = c->DP;
+    a.cap = c->cap;
+    return a;
 }
 
 int sync_if_host(int where, cudaStream_t st) {
@@ -441,6 +454,12 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
     cudaMemset(c->ctr, 0, sizeof(Counters));
     cudaMemset(c->ins_ticket, 0, sizeof(int));
     cudaMemset(c->ws_mem, 0, c->ws_bytes);
+    if (cfg->group_index) {
+        c->gi = new lvg::GroupIndex();
+        if ((e = lvg::create(*c->gi, cfg->d, cfg->S, cfg->r, cfg->grouping, cfg->enclosure, cfg->rng_seed, c->slots,
+                             c->cap)) != cudaSuccess)
+            return cleanup("alloc grouped index", e);
+    }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup("init", e);
     *out = c;
     return LV_OK;
@@ -456,6 +475,10 @@ int lv_destroy(lv_ctx* c) {
     cudaFree(c->ins_ticket);
     cudaFree(c->ws_mem);
     if (c->stage) cudaFree(c->stage);
+    if (c->gi) {
+        lvg::destroy(*c->gi);
+        delete c->gi;
+    }
     delete c;
     return LV_OK;
 }
@@ -544,6 +567,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     const size_t wsb = carve(&probe_geo, nullptr, nullptr);
     if ((e = cudaMalloc(&ws, wsb)) != cudaSuccess) return undo(e);
     cudaMemset(ws, 0, wsb);
+    if (c->gi && (e = lvg::reserve(*c->gi, ncap, st)) != cudaSuccess) return undo(e);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return undo(e);
     cudaFree(c->K);
     cudaFree(c->V);
@@ -591,6 +615,12 @@ int lv_build(lv_ctx* c, const void* K, const void* V, int64_t n, int src_dtype, 
         if (tmp) cudaFreeAsync(tmp, st);
         if (rc) return rc;
         if (int rc2 = launch_summaries(c, 0, (n + c->r - 1) / c->r, n, st)) return rc2;
+    }
+    if (c->gi) {  // build_index over [0, n) (index.cpp:213-221)
+        c->gi->indexed = 0;
+        c->gi->K = 0;
+        LV_CUDA(cudaMemsetAsync(c->gi->nbound, 0, sizeof(unsigned long long) * c->slots * c->gi->S, st));
+        LV_CUDA(lvg::index_range(*c->gi, arena_view(c), 0, n, st));
     }
     Counters h{n, n, 0, 0};
     LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
@@ -644,7 +674,8 @@ int lv_push_key(lv_ctx* c, const void* k, const void* v, int src_dtype, int wher
     if (tmp) LV_CUDA(cudaFreeAsync(tmp, st));
     if (int rc = sync_if_host(where, st)) return rc;
     c->n += 1;
-    if (c->n - c->indexed >= B) {
+    if (c->n - c->indexed >= B) {  // the insert kernel flushed (cache.cpp:7-10)
+        if (c->gi) LV_CUDA(lvg::index_range(*c->gi, arena_view(c), c->indexed, c->n - c->indexed, st));
         c->indexed = c->n;
         c->flushes += 1;
     }
@@ -670,6 +701,7 @@ int lv_flush(lv_ctx* c, void* stream) {
     // into its cell), so folding the buffer into the index is a counter move.
     Counters h{c->n, c->n, c->flushes + 1, 0};
     LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)));
+    if (c->gi) LV_CUDA(lvg::index_range(*c->gi, arena_view(c), c->indexed, c->n - c->indexed, S(stream)));
     LV_CUDA(cudaStreamSynchronize(S(stream)));
     c->indexed = c->n;
     c->flushes += 1;
@@ -1307,9 +1339,53 @@ int lv_load_dataset(const char* path, float* out, int64_t cap_rows, int64_t* n, 
 // The device index of a slot written as the reference's index snapshot: one subspace,
 // contiguous groups of r keys (the device cells) over [0, indexed_count), each with its
 // exact AABB (column min / max of the stored keys, index.cpp:112-117) and members.
+// save_index (io.cpp:236-268) of the grouped index of one slot
+int save_grouped(const lv_ctx* c, int slot, const char* path) {
+    const lvg::GroupIndex& g = *c->gi;
+    const int64_t m = g.indexed, K = g.K;
+    std::ofstream os(path, std::ios::binary);
+    if (!os) return fail(LV_ERUNTIME, std::string("cannot open for writing: ") + path);
+    os.write(kLVIX, 4);
+    put_le<uint32_t>(os, 1);
+    put_le<uint32_t>(os, (uint32_t)c->cfg.d);
+    put_le<uint32_t>(os, (uint32_t)g.S);
+    put_le<uint32_t>(os, (uint32_t)c->cfg.r);
+    put_le<uint32_t>(os, (uint32_t)c->cfg.grouping);
+    put_le<uint32_t>(os, (uint32_t)c->cfg.enclosure);
+    put_le<uint64_t>(os, c->cfg.rng_seed);
+    put_le<uint64_t>(os, (uint64_t)m);
+    std::vector<uint32_t> asg(std::max<int64_t>(m, 1)), off(K + 1), mem(std::max<int64_t>(m, 1));
+    std::vector<float> a((size_t)g.wmax * std::max<int64_t>(K, 1)), b(a.size()), rad(std::max<int64_t>(K, 1));
+    for (int s = 0; s < g.S; ++s) {
+        const int w = g.off[s + 1] - g.off[s];
+        if (lvg::export_subspace(g, slot, s, asg.data(), off.data(), mem.data(), a.data(), b.data(), rad.data(),
+                                 nullptr) != cudaSuccess)
+            return fail(LV_ERUNTIME, "save_index: reading the grouped index");
+        put_le<uint64_t>(os, (uint64_t)m);
+        os.write(reinterpret_cast<const char*>(asg.data()), (std::streamsize)(m * 4));
+        put_le<uint32_t>(os, (uint32_t)K);
+        for (int64_t gg = 0; gg < K; ++gg) {
+            put_le<uint32_t>(os, (uint32_t)c->cfg.enclosure);
+            put_le<uint32_t>(os, (uint32_t)w);
+            for (int i = 0; i < w; ++i) put_le<float>(os, a[(size_t)i * K + gg]);
+            if (c->cfg.enclosure == 1) {
+                put_le<uint32_t>(os, (uint32_t)w);
+                for (int i = 0; i < w; ++i) put_le<float>(os, b[(size_t)i * K + gg]);
+            } else {
+                put_le<float>(os, rad[gg]);
+            }
+            put_le<uint32_t>(os, off[gg + 1] - off[gg]);
+            os.write(reinterpret_cast<const char*>(mem.data() + off[gg]), (std::streamsize)(off[gg + 1] - off[gg]) * 4);
+        }
+    }
+    if (!os) return fail(LV_ERUNTIME, std::string("write failed: ") + path);
+    return LV_OK;
+}
+
 int lv_save_index(const lv_ctx* c, int slot, const char* path) {
     if (!c || !path) return fail(LV_EINVAL, "save_index: null argument");
     if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "save_index: slot out of range");
+    if (c->gi) return save_grouped(c, slot, path);
     const int d = c->cfg.d, r = c->r;
     const int64_t m = c->indexed;
     std::vector<float> rows((size_t)std::max<int64_t>(m, 1) * d);
@@ -1374,6 +1450,21 @@ int lv_load_index(lv_ctx* c, const char* path, int64_t* indexed_count, void* str
     if ((int)d != c->cfg.d) return fail(LV_EINVAL, "load_index: snapshot dimension differs from the cache");
     if (nsub < 1 || nsub > d) return fail(LV_ERUNTIME, "corrupt file: subspace count");
     if ((int64_t)m > c->n) return fail(LV_EINVAL, "load_index: indexed_count exceeds the stored keys");
+    // the grouped index takes the snapshot's groups when it describes this cache's
+    // BuildConfig (one slot); otherwise it is rebuilt over [0, indexed_count) after the load
+    lvg::GroupIndex* gi = c->gi && c->slots == 1 && (int)nsub == c->gi->S && (int)r == c->cfg.r &&
+                                  (int)grouping == c->cfg.grouping && (int)enclosing == c->cfg.enclosure &&
+                                  seed == c->cfg.rng_seed
+                              ? c->gi
+                              : nullptr;
+    // grouped index: every subspace's arrays, as append_gate_entry packs them (index.cpp:139-168)
+    struct Sub {
+        std::vector<uint32_t> asg, off{0}, mem;
+        std::vector<std::vector<float>> a, b;
+        std::vector<float> rad;
+        double nb = 0.0;
+    };
+    std::vector<Sub> subs(gi ? nsub : 0);
     std::vector<uint32_t> asg, mem;
     std::vector<uint8_t> seen;
     for (uint32_t s = 0; s < nsub; ++s) {
@@ -1386,17 +1477,53 @@ int lv_load_index(lv_ctx* c, const char* path, int64_t* indexed_count, void* str
         uint32_t gcount;
         if (!get_le(is, &gcount)) return fail(LV_ERUNTIME, "corrupt file: truncated group count");
         seen.assign(m, 0);
+        const int w = (int)(d / nsub + (s < d % nsub ? 1 : 0));
+        if (gi) {
+            subs[s].asg = asg;
+            subs[s].a.assign(w, {});
+            subs[s].b.assign(w, {});
+        }
         for (uint32_t g = 0; g < gcount; ++g) {
             uint32_t kind, len;
             if (!get_le(is, &kind)) return fail(LV_ERUNTIME, "corrupt file: truncated kind");
             const int nvec = kind == 1 ? 2 : 1;  // Aabb: lo, hi; Ball / SpanBall: center (+ radius)
+            std::vector<float> vec[2];
             for (int v = 0; v < nvec; ++v) {
                 if (!get_le(is, &len)) return fail(LV_ERUNTIME, "corrupt file: truncated vector length");
-                is.seekg((std::streamoff)len * 4, std::ios::cur);
+                if (gi) {
+                    if ((int)len != w || kind != enclosing) return fail(LV_ERUNTIME, "corrupt file: enclosure shape");
+                    vec[v].resize(len);
+                    is.read(reinterpret_cast<char*>(vec[v].data()), (std::streamsize)len * 4);
+                } else {
+                    is.seekg((std::streamoff)len * 4, std::ios::cur);
+                }
             }
+            float rad = 0.0f;
             if (kind != 1) {
-                float rad;
                 if (!get_le(is, &rad)) return fail(LV_ERUNTIME, "corrupt file: truncated radius");
+            }
+            if (gi) {  // append_gate_entry: packed arrays and the norm bound
+                Sub& sb = subs[s];
+                double bnd = 0.0;
+                for (int i = 0; i < w; ++i) {
+                    sb.a[i].push_back(vec[0][i]);
+                    if (kind == 1) sb.b[i].push_back(vec[1][i]);
+                }
+                if (kind == 1) {
+                    double sq = 0.0;
+                    for (int i = 0; i < w; ++i) {
+                        const double x = std::abs(double(vec[0][i])), y = std::abs(double(vec[1][i]));
+                        const double mx = std::max(x, y);
+                        sq += mx * mx;
+                    }
+                    bnd = std::sqrt(sq);
+                } else {
+                    float sq = 0.0f;
+                    for (int i = 0; i < w; ++i) sq += vec[0][i] * vec[0][i];
+                    bnd = double(std::sqrt(sq)) + double(rad);
+                    sb.rad.push_back(rad);
+                }
+                sb.nb = std::max(sb.nb, bnd);
             }
             uint32_t msz;
             if (!get_le(is, &msz)) return fail(LV_ERUNTIME, "corrupt file: truncated member count");
@@ -1407,17 +1534,105 @@ int lv_load_index(lv_ctx* c, const char* path, int64_t* indexed_count, void* str
                 if (id >= m || seen[id] || asg[id] != g) return fail(LV_ERUNTIME, "corrupt file: groups do not partition the indexed keys");
                 seen[id] = 1;
             }
+            if (gi) {
+                subs[s].mem.insert(subs[s].mem.end(), mem.begin(), mem.end());
+                subs[s].off.push_back((uint32_t)subs[s].mem.size());
+            }
         }
         for (uint64_t j = 0; j < m; ++j)
             if (!seen[j]) return fail(LV_ERUNTIME, "corrupt file: groups do not partition the indexed keys");
     }
     if (!at_eof(is)) return fail(LV_ERUNTIME, std::string("corrupt file: trailing bytes in ") + path);
     std::lock_guard<std::mutex> lock(c->writer);
+    if (gi) {
+        for (uint32_t s = 0; s < nsub; ++s) {
+            const Sub& sb = subs[s];
+            const int64_t K = (int64_t)sb.off.size() - 1;
+            const int w = (int)sb.a.size();
+            std::vector<float> a((size_t)w * std::max<int64_t>(K, 1)), b(a.size());
+            for (int i = 0; i < w; ++i)
+                for (int64_t g = 0; g < K; ++g) {
+                    a[(size_t)i * K + g] = sb.a[i][g];
+                    if (enclosing == 1) b[(size_t)i * K + g] = sb.b[i][g];
+                }
+            if (s > 0 && K != gi->K) return fail(LV_ERUNTIME, "load_index: subspaces with different group counts");
+            if (lvg::import_subspace(*gi, 0, (int)s, (long long)m, K, sb.asg.data(), sb.off.data(), sb.mem.data(),
+                                     a.data(), b.data(), sb.rad.data(), sb.nb) != cudaSuccess)
+                return fail(LV_ERUNTIME, "load_index: writing the grouped index");
+        }
+    } else if (c->gi) {
+        c->gi->indexed = 0;
+        c->gi->K = 0;
+        LV_CUDA(cudaMemsetAsync(c->gi->nbound, 0, sizeof(unsigned long long) * c->slots * c->gi->S, S(stream)));
+        LV_CUDA(lvg::index_range(*c->gi, arena_view(c), 0, (long long)m, S(stream)));
+    }
     Counters h{c->n, (long long)m, c->flushes, 0};
     LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)));
     LV_CUDA(cudaStreamSynchronize(S(stream)));
     c->indexed = (long long)m;
     if (indexed_count) *indexed_count = (int64_t)m;
+    return LV_OK;
+}
+
+int lv_group_candidates(lv_ctx* c, int slot, const float* q, float tau, const float* tau_subspace, int algo,
+                        uint32_t* live_bits, uint32_t* live_ids, int64_t cap, int64_t* nlive, lv_group_stats* stats,
+                        void* stream) {
+    if (!c || !q) return fail(LV_EINVAL, "group candidates: null argument");
+    if (!c->gi) return fail(LV_EINVAL, "group candidates: the cache has no grouped index (lv_config.group_index)");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "group candidates: slot out of range");
+    if (algo != LV_ALGO_FULL_SUBSPACE && algo != LV_ALGO_TA) return fail(LV_EINVAL, "group candidates: algo");
+    if (algo == LV_ALGO_FULL_SUBSPACE && !tau_subspace)
+        return fail(LV_EINVAL, "query_full_subspace: tau_subspace required");  // query.cpp:85-86
+    std::lock_guard<std::mutex> lock(c->writer);
+    cudaStream_t st = S(stream);
+    const long long words = std::max<long long>(1, (c->gi->indexed + 31) / 32);
+    uint32_t* bits = live_bits;
+    if (!bits) LV_CUDA(cudaMallocAsync(&bits, sizeof(uint32_t) * words, st));
+    lvg::Stats sg;
+    const cudaError_t e = lvg::candidates(*c->gi, slot, q, tau, tau_subspace, algo == LV_ALGO_TA ? 1 : 0, bits, &sg, st);
+    int rc = LV_OK;
+    if (e != cudaSuccess) rc = fail(LV_ERUNTIME, std::string("group candidates: ") + cudaGetErrorString(e));
+    if (!rc && (live_ids || nlive)) {
+        std::vector<uint32_t> hb(words);
+        if (cudaMemcpy(hb.data(), bits, sizeof(uint32_t) * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(LV_ERUNTIME, "group candidates: reading the live set");
+        int64_t k = 0;
+        for (long long w = 0; w < words && !rc; ++w)
+            for (uint32_t x = hb[w]; x; x &= x - 1) {
+                if (live_ids && k < cap) live_ids[k] = (uint32_t)(w * 32 + __builtin_ctz(x));
+                ++k;
+            }
+        if (nlive) *nlive = k;
+    }
+    if (!live_bits) cudaFreeAsync(bits, st);
+    if (stats && !rc) {
+        stats->groups_tested = sg.groups_tested;
+        stats->keys_scanned = sg.keys_scanned;
+        stats->f_scan = sg.f_scan;
+        stats->gate_cost_equiv = sg.gate_cost_equiv;
+        stats->ta_stop_depth = sg.ta_stop_depth;
+        stats->ta_stop_upper = sg.ta_stop_upper;
+    }
+    return rc;
+}
+
+int lv_group_thresholds(lv_ctx* c, int slot, const float* q, float tau, float* out, void* stream) {
+    if (!c || !q || !out) return fail(LV_EINVAL, "derive_subspace_thresholds: null argument");
+    if (!c->gi) return fail(LV_EINVAL, "derive_subspace_thresholds: the cache has no grouped index");
+    if (slot < 0 || slot >= c->slots) return fail(LV_ERANGE, "derive_subspace_thresholds: slot out of range");
+    std::lock_guard<std::mutex> lock(c->writer);
+    LV_CUDA(lvg::thresholds(*c->gi, slot, q, tau, out, S(stream)));
+    return LV_OK;
+}
+
+int64_t lv_group_count(const lv_ctx* c) { return c && c->gi ? c->gi->K : 0; }
+
+int lv_group_export(const lv_ctx* c, int slot, int s, uint32_t* assignments, uint32_t* member_offsets,
+                    uint32_t* member_ids, float* a, float* b, float* radii, double* norm_bound) {
+    if (!c) return fail(LV_EINVAL, "group export: null context");
+    if (!c->gi) return fail(LV_EINVAL, "group export: the cache has no grouped index");
+    if (slot < 0 || slot >= c->slots || s < 0 || s >= c->gi->S) return fail(LV_ERANGE, "group export: slot or subspace");
+    LV_CUDA(lvg::export_subspace(*c->gi, slot, s, assignments, member_offsets, member_ids, a, b, radii, norm_bound));
     return LV_OK;
 }
 

@@ -96,6 +96,26 @@ class QueryStats:
 
 
 @dataclasses.dataclass
+class CandidateSet:
+    """query.hpp:34-37: live ids (ascending, duplicate-free) and the filter's statistics."""
+    live_ids: np.ndarray
+    stats: QueryStats
+
+
+@dataclasses.dataclass
+class SubspaceIndex:
+    """One subspace of the grouped index (index.hpp:29-52), copied from the device."""
+    assignments: np.ndarray            # key id -> group id
+    member_offsets: np.ndarray         # [K + 1]
+    member_ids: np.ndarray             # group g: member_ids[member_offsets[g]:member_offsets[g + 1]]
+    gate_centers: Optional[np.ndarray]  # [w][K] (ball kinds)
+    gate_radii: Optional[np.ndarray]    # [K]
+    gate_lo: Optional[np.ndarray]       # [w][K] (AABB)
+    gate_hi: Optional[np.ndarray]
+    norm_bound: float
+
+
+@dataclasses.dataclass
 class AttentionResult:
     selected_ids: np.ndarray           # attended token ids, ascending
     weights: Optional[np.ndarray]      # aligned with selected_ids (when requested)
@@ -110,11 +130,11 @@ class CacheQueryResult:
     attention: Optional[AttentionResult]
 
 
-def _config(d, heads, group, batch, dtype, cfg: BuildConfig, B, capacity) -> _capi.lv_config:
+def _config(d, heads, group, batch, dtype, cfg: BuildConfig, B, capacity, group_index=False) -> _capi.lv_config:
     return _capi.lv_config(
         d=d, n_kv_heads=heads, group_size=group, batch=batch, dtype=dtype, S=cfg.S, r=cfg.r,
         grouping=_GROUPING.get(cfg.grouping, -1), enclosure=_ENCLOSURE.get(cfg.enclosing, -1),
-        rng_seed=cfg.rng_seed, buffer_capacity=B, capacity=capacity,
+        rng_seed=cfg.rng_seed, buffer_capacity=B, capacity=capacity, group_index=1 if group_index else 0,
     )
 
 
@@ -186,26 +206,31 @@ class LouverCache:
     grows geometrically like KeyStore (core.hpp:134-142).
     """
 
-    def __init__(self, dim: int, cfg: BuildConfig, buffer_capacity: int, capacity: int = 1024):
+    def __init__(self, dim: int, cfg: BuildConfig, buffer_capacity: int, capacity: int = 1024,
+                 group_index: bool = True):
         cfg.validate(dim)
         if buffer_capacity < 1:
             raise ValueError("LouverCache: buffer capacity >= 1 required")
         self.d = dim
         self.cfg = cfg
         self.B = int(buffer_capacity)
-        self._ctx = _Context(_config(dim, 1, 1, 1, LV_F32, cfg, self.B, max(capacity, 16)))
+        # group_index: the reference's LouverIndex for cfg (PCA tree, balls, S subspaces ...)
+        # is also built on the device; it supplies query()'s QueryStats and candidate sets
+        self.group_index = bool(group_index)
+        self._ctx = _Context(_config(dim, 1, 1, 1, LV_F32, cfg, self.B, max(capacity, 16), self.group_index))
         self._cap = max(capacity, 16)
         self._pool_lock = threading.Lock()
         self._pool = []  # (bits, totals) device scratch leased by queries
 
     @classmethod
-    def adopt(cls, keys: np.ndarray, values: np.ndarray, cfg: BuildConfig, buffer_capacity: int):
+    def adopt(cls, keys: np.ndarray, values: np.ndarray, cfg: BuildConfig, buffer_capacity: int,
+              group_index: bool = True):
         keys = np.ascontiguousarray(keys, dtype=np.float32)
         values = np.ascontiguousarray(values, dtype=np.float32)
         if keys.shape != values.shape or keys.ndim != 2:
             raise ValueError("KeyStore: keys/values shape mismatch")
         n, d = keys.shape
-        self = cls(d, cfg, buffer_capacity, capacity=max(2 * n, 1024))
+        self = cls(d, cfg, buffer_capacity, capacity=max(2 * n, 1024), group_index=group_index)
         if n:
             check(self._ctx.lib.lv_build(self._ctx.h, _ptr(keys), _ptr(values), n, LV_F32, LV_HOST,
                                          None), "lv_build")
@@ -287,9 +312,18 @@ class LouverCache:
             self._release(bits, totals)
         retrieved = np.concatenate([selected[selected < indexed],
                                     np.arange(indexed, n, dtype=np.uint32)]).astype(np.uint32)
-        stats = QueryStats(groups_tested=int(tot[0]), keys_scanned=int(counts[2]),
-                           f_scan=(counts[2] / n) if n else 1.0,
-                           gate_cost_equiv=2.0 * float(tot[0]) / max(1, self.cfg.r))
+        if self.group_index:
+            # the reference's statistics (cache.cpp:37-64): the filter's on the grouped index,
+            # then the buffer counted as scanned and f_scan over every stored key
+            stats = QueryStats()
+            if indexed:
+                stats = _group_candidates(self, req, algo, want_ids=False).stats
+            stats.keys_scanned += n - indexed
+            stats.f_scan = (stats.keys_scanned / n) if n else 1.0
+        else:
+            stats = QueryStats(groups_tested=int(tot[0]), keys_scanned=int(counts[2]),
+                               f_scan=(counts[2] / n) if n else 1.0,
+                               gate_cost_equiv=2.0 * float(tot[0]) / max(1, self.cfg.r))
         attention = None
         if counts[3]:
             attended = np.ascontiguousarray(selected if strict_threshold else retrieved, dtype=np.uint32)
@@ -300,6 +334,27 @@ class LouverCache:
                                                          LV_HOST, _ptr(weights), None), "attention weights")
             attention = AttentionResult(selected_ids=attended, weights=weights[: attended.size], output=out)
         return CacheQueryResult(selected=selected, retrieved=retrieved, stats=stats, attention=attention)
+
+    def index_subspace(self, s: int) -> SubspaceIndex:
+        """Subspace s of the grouped index (index.hpp:29-52), copied to the host."""
+        if not self.group_index:
+            raise ValueError("LouverCache: built without the grouped index")
+        n, K = self.indexed_count(), int(self._ctx.lib.lv_group_count(self._ctx.h))
+        w = self.d // self.cfg.S + (1 if s < self.d % self.cfg.S else 0)
+        asg = np.zeros((max(n, 1),), np.uint32)
+        off = np.zeros((K + 1,), np.uint32)
+        mem = np.zeros((max(n, 1),), np.uint32)
+        a = np.zeros((w, max(K, 1)), np.float32)
+        b = np.zeros((w, max(K, 1)), np.float32)
+        rad = np.zeros((max(K, 1),), np.float32)
+        nb = C.c_double(0.0)
+        check(self._ctx.lib.lv_group_export(self._ctx.h, 0, s, _ptr(asg), _ptr(off), _ptr(mem), _ptr(a), _ptr(b),
+                                            _ptr(rad), C.byref(nb)), "lv_group_export")
+        a, b, rad = a[:, :K].copy(), b[:, :K].copy(), rad[:K].copy()
+        aabb = self.cfg.enclosing == "aabb"
+        return SubspaceIndex(assignments=asg[:n], member_offsets=off, member_ids=mem[:n],
+                             gate_centers=None if aabb else a, gate_radii=None if aabb else rad,
+                             gate_lo=a if aabb else None, gate_hi=b if aabb else None, norm_bound=nb.value)
 
     def _lease(self):
         torch = _torch()
@@ -315,6 +370,58 @@ class LouverCache:
     def _release(self, bits, totals):
         with self._pool_lock:
             self._pool.append((bits, totals))
+
+
+def _group_candidates(cache: LouverCache, req: QueryRequest, algo: FilterAlgo, want_ids: bool = True) -> CandidateSet:
+    if not cache.group_index:
+        raise ValueError("LouverCache: built without the grouped index")
+    q = np.ascontiguousarray(req.q, dtype=np.float32).reshape(-1)
+    if q.size != cache.d:
+        raise ValueError("dot: length mismatch")
+    ts = None
+    if algo == FilterAlgo.FullSubspace:
+        if req.tau_subspace is None:  # cache.cpp:38-41
+            ts = derive_subspace_thresholds(cache, q, req.tau)
+        else:
+            ts = np.ascontiguousarray(req.tau_subspace, dtype=np.float32)
+            if ts.size != cache.cfg.S:
+                raise ValueError("query_full_subspace: tau_subspace length != S")
+    n = cache.indexed_count()
+    ids = np.zeros((max(n, 1),), np.uint32) if want_ids else None
+    nlive = C.c_int64(0)
+    st = _capi.lv_group_stats()
+    check(cache._ctx.lib.lv_group_candidates(cache._ctx.h, 0, _ptr(q), float(np.float32(req.tau)),
+                                             _ptr(ts), int(algo), None, _ptr(ids), n, C.byref(nlive), C.byref(st),
+                                             None), "group candidates")
+    stats = QueryStats(groups_tested=int(st.groups_tested), keys_scanned=int(st.keys_scanned), f_scan=st.f_scan,
+                       gate_cost_equiv=st.gate_cost_equiv,
+                       ta_stop_depth=None if st.ta_stop_depth < 0 else int(st.ta_stop_depth),
+                       ta_stop_upper=None if st.ta_stop_depth < 0 else float(st.ta_stop_upper))
+    live = ids[: nlive.value].copy() if want_ids else np.zeros((0,), np.uint32)
+    return CandidateSet(live_ids=live, stats=stats)
+
+
+def query_ta(cache: LouverCache, req: QueryRequest) -> CandidateSet:
+    """query.hpp:60-63 on the device grouped index (query.cpp:204-303)."""
+    return _group_candidates(cache, req, FilterAlgo.Ta)
+
+
+def query_full_subspace(cache: LouverCache, req: QueryRequest) -> CandidateSet:
+    """query.hpp:56-58 on the device grouped index (query.cpp:82-117); tau_subspace required."""
+    if req.tau_subspace is None:
+        raise ValueError("query_full_subspace: tau_subspace required")
+    return _group_candidates(cache, req, FilterAlgo.FullSubspace)
+
+
+def derive_subspace_thresholds(cache: LouverCache, q, tau: float) -> np.ndarray:
+    """query.hpp:65-67 on the device grouped index (query.cpp:305-336)."""
+    if not cache.group_index:
+        raise ValueError("LouverCache: built without the grouped index")
+    q = np.ascontiguousarray(q, dtype=np.float32).reshape(-1)
+    out = np.zeros((cache.cfg.S,), np.float32)
+    check(cache._ctx.lib.lv_group_thresholds(cache._ctx.h, 0, _ptr(q), float(np.float32(tau)), _ptr(out), None),
+          "derive_subspace_thresholds")
+    return out
 
 
 def brute_force_range(cache: LouverCache, q, tau: float, limit: Optional[int] = None) -> np.ndarray:

@@ -137,7 +137,7 @@ class KeyStore {
 struct QueryRequest {
     Vector q;
     Scalar tau = 0.0f;
-    std::optional<std::vector<Scalar>> tau_subspace;  // accepted; the device probe derives its own bounds
+    std::optional<std::vector<Scalar>> tau_subspace;  // full-subspace filter (grouped index); else derived
     Scalar scale = 0.0f;                              // 0 means 1/sqrt(d)
 
     Scalar effective_scale() const {
@@ -145,12 +145,16 @@ struct QueryRequest {
     }
 };
 
-// query.hpp:21-30 (device meaning: groups = cells of r keys)
+// query.hpp:21-30. With the grouped index (the default for LouverCache) these are the
+// reference's statistics for the BuildConfig; without it, groups are the device cells.
 struct QueryStats {
-    std::int64_t groups_tested = 0;  // cells whose bound was evaluated
-    std::int64_t keys_scanned = 0;   // keys entering the exact check (surviving cells + buffer)
-    double f_scan = 0.0;             // keys_scanned / n
-    double gate_cost_equiv = 0.0;    // 2 * groups_tested / r (AABB: hi and lo rows)
+    std::vector<std::int64_t> groups_tested_per_subspace;
+    std::int64_t groups_tested = 0;  // groups whose bound was evaluated (sum over subspaces)
+    std::int64_t keys_scanned = 0;   // keys entering the exact check (+ the buffer at cache level)
+    double f_scan = 0.0;             // keys_scanned / indexed_count (cache level: / n)
+    double gate_cost_equiv = 0.0;    // g * groups_tested / r (g = 2 for AABB, 1 for balls)
+    std::optional<int> ta_stop_depth;
+    std::optional<double> ta_stop_upper;
 };
 
 // query.hpp:37-41
@@ -189,16 +193,20 @@ struct IndexView {
 // concurrently (each call uses its own device workspace).
 class LouverCache {
   public:
-    LouverCache(int dim, BuildConfig cfg, std::size_t buffer_capacity, std::size_t capacity = 1024)
-        : dim_(dim), cfg_(cfg), buffer_capacity_(buffer_capacity) {
+    // group_index: also build the reference's LouverIndex for cfg on the device (PCA tree,
+    // enclosures, S subspaces); it supplies QueryStats, query_ta / query_full_subspace's
+    // candidate sets and derive_subspace_thresholds exactly as the reference computes them.
+    LouverCache(int dim, BuildConfig cfg, std::size_t buffer_capacity, std::size_t capacity = 1024,
+                bool group_index = true)
+        : dim_(dim), cfg_(cfg), buffer_capacity_(buffer_capacity), group_index_(group_index) {
         cfg.validate(dim);
         if (buffer_capacity < 1) throw std::invalid_argument("LouverCache: buffer capacity >= 1 required");
         create(capacity < 16 ? 16 : capacity);
     }
 
     // Adopts an existing store; all of it is indexed immediately (cache.hpp:31-36).
-    LouverCache(const KeyStore& store, BuildConfig cfg, std::size_t buffer_capacity)
-        : dim_(store.dim()), cfg_(cfg), buffer_capacity_(buffer_capacity) {
+    LouverCache(const KeyStore& store, BuildConfig cfg, std::size_t buffer_capacity, bool group_index = true)
+        : dim_(store.dim()), cfg_(cfg), buffer_capacity_(buffer_capacity), group_index_(group_index) {
         if (buffer_capacity < 1) throw std::invalid_argument("LouverCache: buffer capacity >= 1 required");
         cfg.validate(dim_);
         create(store.n() * 2 < 1024 ? 1024 : store.n() * 2);
@@ -250,12 +258,18 @@ class LouverCache {
         for (KeyId id : r.selected)
             if (id < indexed) r.retrieved.push_back(id);
         for (int64_t j = indexed; j < n_now; ++j) r.retrieved.push_back(static_cast<KeyId>(j));
-        uint64_t tot[4] = {0, 0, 0, 0};
-        detail::cuda_check(cudaMemcpy(tot, sc->totals(), sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
-        r.stats.groups_tested = static_cast<int64_t>(tot[0]);
-        r.stats.keys_scanned = counts[2];
-        r.stats.f_scan = n_now ? double(counts[2]) / double(n_now) : 1.0;
-        r.stats.gate_cost_equiv = 2.0 * double(tot[0]) / double(cfg_.r);
+        if (group_index_) {  // cache.cpp:37-64: the filter's stats, then the buffer and f_scan over n
+            if (indexed > 0) r.stats = group_candidates(req, algo, false).stats;
+            r.stats.keys_scanned += n_now - indexed;
+            r.stats.f_scan = n_now ? double(r.stats.keys_scanned) / double(n_now) : 1.0;
+        } else {
+            uint64_t tot[4] = {0, 0, 0, 0};
+            detail::cuda_check(cudaMemcpy(tot, sc->totals(), sizeof(tot), cudaMemcpyDeviceToHost), "cudaMemcpy");
+            r.stats.groups_tested = static_cast<int64_t>(tot[0]);
+            r.stats.keys_scanned = counts[2];
+            r.stats.f_scan = n_now ? double(counts[2]) / double(n_now) : 1.0;
+            r.stats.gate_cost_equiv = 2.0 * double(tot[0]) / double(cfg_.r);
+        }
         if (counts[3]) {
             AttentionResult att{strict_threshold ? r.selected : r.retrieved, {}, std::move(out)};
             att.weights.resize(att.selected_ids.size());
@@ -295,6 +309,58 @@ class LouverCache {
         c.groups_tested = static_cast<int64_t>(tot[0]);
         return c;
     }
+
+    struct GroupCandidates {
+        std::vector<KeyId> live_ids;
+        QueryStats stats;
+    };
+    // query_ta / query_full_subspace (query.cpp:82-303) on the grouped index: the reference's
+    // candidate set and statistics. FullSubspace takes req.tau_subspace, else derives it
+    // (cache.cpp:38-41).
+    GroupCandidates group_candidates(const QueryRequest& req, FilterAlgo algo, bool want_ids = true) const {
+        if (!group_index_) throw std::invalid_argument("LouverCache: built without the grouped index");
+        if (req.q.size() != static_cast<size_t>(dim_)) throw std::invalid_argument("dot: length mismatch");
+        std::vector<Scalar> ts;
+        if (algo == FilterAlgo::FullSubspace) {
+            if (req.tau_subspace) {
+                if (static_cast<int>(req.tau_subspace->size()) != cfg_.S)
+                    throw std::invalid_argument("query_full_subspace: tau_subspace length != S");
+                ts = *req.tau_subspace;
+            } else {
+                ts = group_thresholds(req.q, req.tau);
+            }
+        }
+        const int64_t m = static_cast<int64_t>(indexed_count());
+        GroupCandidates out;
+        if (want_ids) out.live_ids.resize(static_cast<size_t>(m));
+        int64_t nlive = 0;
+        lv_group_stats st{};
+        detail::check(lv_group_candidates(ctx_.get(), 0, req.q.data(), req.tau, ts.empty() ? nullptr : ts.data(),
+                                          static_cast<int>(algo), nullptr, want_ids ? out.live_ids.data() : nullptr, m,
+                                          &nlive, &st, nullptr),
+                      "group candidates");
+        if (want_ids) out.live_ids.resize(static_cast<size_t>(nlive));
+        out.stats.groups_tested_per_subspace.assign(static_cast<size_t>(cfg_.S), lv_group_count(ctx_.get()));
+        out.stats.groups_tested = st.groups_tested;
+        out.stats.keys_scanned = st.keys_scanned;
+        out.stats.f_scan = st.f_scan;
+        out.stats.gate_cost_equiv = st.gate_cost_equiv;
+        if (st.ta_stop_depth >= 0) {
+            out.stats.ta_stop_depth = st.ta_stop_depth;
+            out.stats.ta_stop_upper = st.ta_stop_upper;
+        }
+        return out;
+    }
+    // derive_subspace_thresholds (query.cpp:305-336) on the grouped index
+    std::vector<Scalar> group_thresholds(ConstVecRef q, Scalar tau) const {
+        if (!group_index_) throw std::invalid_argument("LouverCache: built without the grouped index");
+        if (q.size() != static_cast<size_t>(dim_)) throw std::invalid_argument("dot: length mismatch");
+        std::vector<Scalar> out(static_cast<size_t>(cfg_.S));
+        detail::check(lv_group_thresholds(ctx_.get(), 0, q.data(), tau, out.data(), nullptr), "derive_subspace_thresholds");
+        return out;
+    }
+    bool has_group_index() const { return group_index_; }
+    const BuildConfig& config() const { return cfg_; }
 
     // cache.hpp:49: a host copy of the device store (KeyStore of the stored rows)
     KeyStore store() const { return KeyStore(rows(false), rows(true), dim_); }
@@ -398,6 +464,7 @@ class LouverCache {
         c.rng_seed = cfg_.rng_seed;
         c.buffer_capacity = static_cast<int64_t>(buffer_capacity_);
         c.capacity = static_cast<int64_t>(capacity);
+        c.group_index = group_index_ ? 1 : 0;
         lv_ctx* h = nullptr;
         detail::check(lv_create(&c, &h), "lv_create");
         ctx_.reset(h);
@@ -406,6 +473,7 @@ class LouverCache {
     int dim_;
     BuildConfig cfg_;
     std::size_t buffer_capacity_;
+    bool group_index_ = true;
     std::size_t capacity_ = 0;
     std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
     mutable std::mutex pool_mu_;
@@ -460,9 +528,13 @@ inline CandidateSet candidate_set(const LouverCache& cache, const QueryRequest& 
 }
 }  // namespace detail
 
-// query.hpp:55-58: the device filter (full-dimension cell bounds against req.tau; the
-// candidate set contains every indexed key with dot(q, k) >= tau).
+// query.hpp:60-63: on the grouped index, the reference's TA candidate set and stats; without
+// it, the device cells' filter (full-dimension cell bounds against req.tau).
 inline CandidateSet query_ta(const LouverCache& cache, const QueryRequest& req) {
+    if (cache.has_group_index()) {
+        auto g = cache.group_candidates(req, FilterAlgo::Ta);
+        return CandidateSet{std::move(g.live_ids), std::move(g.stats)};
+    }
     return detail::candidate_set(cache, req);
 }
 
@@ -472,12 +544,17 @@ inline CandidateSet query_full_subspace(const LouverCache& cache, const QueryReq
     if (!req.tau_subspace) throw std::invalid_argument("query_full_subspace: tau_subspace required");
     if (static_cast<int>(req.tau_subspace->size()) != S)
         throw std::invalid_argument("query_full_subspace: tau_subspace length != S");
+    if (cache.has_group_index() && S == cache.config().S) {  // the reference's filter (query.cpp:82-117)
+        auto g = cache.group_candidates(req, FilterAlgo::FullSubspace);
+        return CandidateSet{std::move(g.live_ids), std::move(g.stats)};
+    }
     return detail::candidate_set(cache, req);
 }
 
 // query.hpp:60-65 over the device index (lv_subspace_thresholds).
 inline std::vector<Scalar> derive_subspace_thresholds(const LouverCache& cache, ConstVecRef q, Scalar tau, int S) {
     if (q.size() != static_cast<size_t>(cache.dim())) throw std::invalid_argument("dot: length mismatch");
+    if (cache.has_group_index() && S == cache.config().S) return cache.group_thresholds(q, tau);  // query.cpp:305-336
     std::vector<Scalar> out(static_cast<size_t>(S > 0 ? S : 0));
     detail::check(lv_subspace_thresholds(cache.handle(), 0, q.data(), tau, S, LV_HOST, out.data(), nullptr),
                   "derive_subspace_thresholds");

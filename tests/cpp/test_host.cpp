@@ -110,8 +110,34 @@ static void test_cache_fp32() {
         std::vector<KeyId> all(n);
         for (int64_t j = 0; j < n; ++j) all[j] = (KeyId)(n - 1 - j);
         EXPECT(exact_check(cache, all, {q, (size_t)d}, tau) == oracle_range(K, n, d, q, tau), "exact_check q%d", qi);
-        // query_ta's candidate set: a superset of the indexed selected keys, within [0, indexed)
-        const CandidateSet cs = query_ta(cache, req);
+        // query_ta's candidate set on the grouped index: the oracle cache's, id for id, with its stats
+        {
+            lvo_build_config oc{4, 16, 3, 0, 0};  // S=4, r=16, PCA tree, ball
+            lvo_cache* oca = nullptr;
+            lvo_cache_adopt(K.data(), V.data(), n0, d, &oc, 64, &oca);
+            for (int64_t j = n0; j < n; ++j) lvo_cache_push_key(oca, K.data() + j * d, V.data() + j * d);
+            std::vector<uint32_t> ids(n);
+            int64_t cnt = 0;
+            lvo_stats ost{};
+            lvo_cache_candidates(oca, q, tau, nullptr, 1, ids.data(), n, &cnt, &ost);
+            ids.resize(cnt);
+            const CandidateSet g = query_ta(cache, req);
+            EXPECT(g.live_ids == ids && g.stats.keys_scanned == ost.keys_scanned &&
+                       g.stats.ta_stop_depth.value_or(-1) == ost.ta_stop_depth,
+                   "query_ta on the grouped index q%d: %zu vs oracle %zu", qi, g.live_ids.size(), ids.size());
+            std::vector<float> ots(4);
+            lvo_cache_thresholds(oca, q, tau, ots.data());
+            EXPECT(derive_subspace_thresholds(cache, {q, (size_t)d}, tau, 4) == ots, "grouped thresholds q%d", qi);
+            QueryRequest rq = req;
+            rq.tau_subspace = ots;
+            ids.assign(n, 0);
+            lvo_cache_candidates(oca, q, tau, ots.data(), 0, ids.data(), n, &cnt, &ost);
+            ids.resize(cnt);
+            EXPECT(query_full_subspace(cache, rq, 4).live_ids == ids, "query_full_subspace on the grouped index q%d", qi);
+            lvo_cache_destroy(oca);
+        }
+        // the device cells' candidate set: a superset of the indexed selected keys, within [0, indexed)
+        const CandidateSet cs = detail::candidate_set(cache, req);
         const auto sel_all = oracle_range(K, n, d, q, tau);
         bool sup = true, inside = true;
         for (KeyId id : sel_all)
@@ -120,7 +146,8 @@ static void test_cache_fp32() {
             if (id >= cache.indexed_count()) inside = false;
         EXPECT(sup && inside && std::is_sorted(cs.live_ids.begin(), cs.live_ids.end()), "query_ta candidates q%d", qi);
         EXPECT(cs.stats.keys_scanned == (int64_t)cs.live_ids.size() && cs.stats.groups_tested > 0, "candidate stats");
-        // derive_subspace_thresholds: S = 1 gives tau itself; S = 4 thresholds are safe for every selected key
+        // derive_subspace_thresholds over the device cells (S other than the grouped index's):
+        // S = 1 gives tau itself; S = 4 thresholds are safe for every selected key
         EXPECT(derive_subspace_thresholds(cache, {q, (size_t)d}, tau, 1)[0] == tau, "S=1 threshold");
         const auto ts = derive_subspace_thresholds(cache, {q, (size_t)d}, tau, 4);
         bool safe = ts.size() == 4;

@@ -472,7 +472,7 @@ class LouverLayer:
 
     def __init__(self, d: int, n_kv_heads: int, group_size: int, batch: int, capacity: int,
                  cfg: Optional[BuildConfig] = None, buffer_capacity: int = 128,
-                 dtype: str = "bf16"):
+                 dtype: str = "bf16", group_index: bool = False):
         cfg = cfg or BuildConfig(S=1, r=16, grouping="contiguous", enclosing="aabb")
         cfg.validate(d)
         self.d, self.H_kv, self.G, self.batch = d, n_kv_heads, group_size, batch
@@ -480,8 +480,9 @@ class LouverLayer:
         self.rows = batch * self.H_q
         self.dtype = LV_BF16 if dtype == "bf16" else LV_F32
         self.cfg = cfg
+        self.group_index = bool(group_index)
         self._ctx = _Context(_config(d, n_kv_heads, group_size, batch, self.dtype, cfg,
-                                     buffer_capacity, capacity))
+                                     buffer_capacity, capacity, self.group_index))
 
     @property
     def n(self) -> int:

@@ -25,7 +25,7 @@
 // the CTA's cells is attended; same pipeline, same score precision.
 //
 // Every block of keys, summaries or values moves global -> shared with cp.async into a
-// per-warp 3-stage ring, 128-byte XOR swizzle (chunk ^ row&7), read with ldmatrix, so no
+// per-warp 3-stage ring, laid out as the TMA 128-byte swizzle (see lay()), read with ldmatrix, so no
 // register holds an in-flight block and the fragments need no register shuffling. Per
 // warp the exact phase is a software pipeline:
 // K(t+1) in flight | K(t) scored | V(t-1) in flight, folded after K(t) is scored.
@@ -81,11 +81,18 @@ __device__ __forceinline__ unsigned row_bits(unsigned b) {
     }
 }
 
-// Byte offset of k-step ks's 16-byte chunk of row a_row in a 128-byte-swizzled stage
-// (chunk c of row r is stored at c ^ (r & 7)): only the low three chunk bits are swizzled,
-// so k-steps 4 apart differ by a constant 128 bytes.
-__device__ __forceinline__ unsigned swz_off(int ks, int a_hi, int a_row) {
-    return ((unsigned)(ks >> 2) << 7) + ((unsigned)(((2 * (ks & 3) + a_hi) ^ (a_row & 7))) << 4);
+// Stage layout (the TMA SWIZZLE_128B image of a 16-row block): 128-byte column halves of
+// 16 rows each, half h at h * 2048; 16-byte chunk c of row r at
+//   (c >> 3) * 2048 + r * 128 + ((c & 7) ^ ((r + b7) & 7)) * 16,
+// b7 = bits 7..9 of the stage's shared address (the hardware swizzle XORs with the
+// absolute address bits), so ldmatrix reads of 8 rows at one chunk are conflict-free.
+__device__ __forceinline__ unsigned lay(int r, int c, int b7) {
+    return ((unsigned)(c >> 3) << 11) + ((unsigned)r << 7) + ((unsigned)((c & 7) ^ ((r + b7) & 7)) << 4);
+}
+// k-step ks's chunk (2 ks + hi) of a row whose swizzle key is rx = (row + b7) & 7,
+// relative to the row start
+__device__ __forceinline__ unsigned swz_off(int ks, int a_hi, int rx) {
+    return ((unsigned)(ks >> 2) << 11) + ((unsigned)(((2 * (ks & 3) + a_hi) ^ rx)) << 4);
 }
 
 template <int DP, int G>
@@ -144,14 +151,17 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     const int blk = blockIdx.x, nb = vp.nb;
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
     const unsigned ring = smem_u32(wbase);
+    const int b7 = (int)((ring >> 7) & 7u);  // the same for every stage of the warp (4 KiB apart)
     float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
     const int q4 = lane & 3;
     // per-lane ldmatrix offsets: A (rows = keys / cells) and V^T (trans)
     const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
-    const unsigned a_off = a_row * RB;
+    const unsigned a_off = a_row * 128;
+    const int a_rx = (a_row + b7) & 7;
     const int v_row = (lane & 7) + 8 * (lane >> 4), v_hi = (lane >> 3) & 1;
-    const unsigned v_off = v_row * RB;
+    const unsigned v_off = v_row * 128;
+    const int v_rx = (v_row + b7) & 7;
 
     // programmatic dependent launch: dispatched early, while the preceding kernel in the
     // stream drains; only immutable data (sealed cell summaries) is read before
@@ -192,7 +202,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
         for (int kk = 0; kk < P0; ++kk) {
             const int row = kk * RPI0 + lane / CPR, c = lane % CPR;
-            pdoff[kk] = row * RB + ((c ^ (row & 7)) << 4);
+            pdoff[kk] = lay(row, c, b7);
         }
         const size_t plane = ((size_t)(lane / CPR) * nb * (4 * DP)) + (size_t)(lane % CPR) * 16;
         const size_t pkstride = (size_t)RPI0 * nb * (4 * DP);
@@ -204,14 +214,14 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (c0 + 15LL * nb < cap_cells) {  // every row inside the arena
                     const unsigned char* src = sumb + (size_t)c0 * (4 * DP) + hoff + plane;
 #pragma unroll
-                    for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P0) * 8 * RB + pdoff[k % P0], src + k * pkstride);
+                    for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P0) * 8 * 128 + pdoff[k % P0], src + k * pkstride);
                 } else {
 #pragma unroll
                     for (int k = 0; k < CPR / 2; ++k) {
                         const int ch = k * 32 + lane, row = ch / CPR, c = ch % CPR;
                         long long cell = c0 + (long long)row * nb;
                         cell = cell < cap_cells ? cell : cap_cells - 1;  // past the arena: any row, ignored
-                        cpa16(dst + row * RB + ((c ^ (row & 7)) << 4), sumb + (size_t)cell * (4 * DP) + hoff + c * 16);
+                        cpa16(dst + lay(row, c, b7), sumb + (size_t)cell * (4 * DP) + hoff + c * 16);
                     }
                 }
             }
@@ -354,8 +364,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int k2 = 0; k2 < KS / 2; ++k2) {
                     unsigned a0[4], a1[4];
-                    ldsm4(a0, sb + swz_off(2 * k2, a_hi, a_row));
-                    ldsm4(a1, sb + swz_off(2 * k2 + 1, a_hi, a_row));
+                    ldsm4(a0, sb + swz_off(2 * k2, a_hi, a_rx));
+                    ldsm4(a1, sb + swz_off(2 * k2 + 1, a_hi, a_rx));
 #pragma unroll
                     for (int nt = 0; nt < NTP; ++nt) {
                         const uint4 b = fh[(k2 * NTP + nt) * 32 + lane];
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
             for (int kk = 0; kk < P; ++kk) {
                 const int row = kk * RPI + lane / CPR, c = lane % CPR;
-                doff[kk] = row * RB + ((c ^ (row & 7)) << 4);
+                doff[kk] = lay(row, c, b7);
             }
             auto k_issue = [&](int t, int kb, int stage) {  // rows past n land as zeros
                 if (t < ntask) {
@@ -466,12 +476,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const unsigned dst = ring + stage * Ge::STAGE;
                     if (kb + 16 <= n32) {  // the common case: the whole block is stored keys
 #pragma unroll
-                        for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512);
+                        for (int k = 0; k < CPR / 2; ++k) cpa16(dst + (k / P) * 8 * 128 + doff[k % P], src + k * 512);
                     } else {
                         const int lim = n32 - kb - lane / CPR;
 #pragma unroll
                         for (int k = 0; k < CPR / 2; ++k)
-                            cpa16z(dst + (k / P) * 8 * RB + doff[k % P], src + k * 512, k * RPI < lim);
+                            cpa16z(dst + (k / P) * 8 * 128 + doff[k % P], src + k * 512, k * RPI < lim);
                     }
                 }
                 cpa_commit();
@@ -506,8 +516,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int k2 = 0; k2 < KS / 2; ++k2) {
                         unsigned a0[4], a1[4];
-                        ldsm4(a0, sb + a_off + swz_off(2 * k2, a_hi, a_row));
-                        ldsm4(a1, sb + a_off + swz_off(2 * k2 + 1, a_hi, a_row));
+                        ldsm4(a0, sb + a_off + swz_off(2 * k2, a_hi, a_rx));
+                        ldsm4(a1, sb + a_off + swz_off(2 * k2 + 1, a_hi, a_rx));
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
                             const uint4 b = fq[(k2 * NT + nt) * 32 + lane];
@@ -543,11 +553,11 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     for (int j = 0; j < PPL; ++j) {
                         if ((und >> j) & 1) {
                             const int rw = (lane + 32 * j) / G;
-                            const unsigned rb = sb + rw * RB;
+                            const unsigned rb = sb;
                             float a2 = 0.0f;
 #pragma unroll 1
                             for (int cc = 0; cc < CPR; ++cc) {
-                                const uint4 kv = lds16(rb + ((cc ^ (rw & 7)) << 4));
+                                const uint4 kv = lds16(rb + lay(rw, cc, b7));
                                 float kf[8];
                                 lvk::unpack16<__nv_bfloat16>(kv, kf);
 #pragma unroll
@@ -637,7 +647,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     const unsigned char* vsrc = reinterpret_cast<const unsigned char*>(Vs + (size_t)k0 * DP) + cc * 16;
                     for (int k = lane / CPR; k < nr; k += RPI) {
                         const int rsel = rows8[k];
-                        cpa16(dst + rsel * RB + ((cc ^ (rsel & 7)) << 4), vsrc + rsel * RB);
+                        cpa16(dst + lay(rsel, cc, b7), vsrc + rsel * RB);
                     }
                 }
                 cpa_commit();
@@ -649,7 +659,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         unsigned a[4];
-                        ldsm4t(a, vb + swz_off(mt, v_hi, v_row));
+                        ldsm4t(a, vb + swz_off(mt, v_hi, v_rx));
                         mma16816(o[mt], a, pb[0], pb[1]);
                         if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                     }
@@ -680,7 +690,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     unsigned a[4];
-                    ldsm4t(a, vb + swz_off(mt, v_hi, v_row));
+                    ldsm4t(a, vb + swz_off(mt, v_hi, v_rx));
                     mma16816(o[mt], a, pb[0], pb[1]);
                     if (!PACK) mma16816(o[mt], a, pb[2], pb[3]);
                 }

@@ -30,6 +30,7 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
         if (nb2 >= nb) break;  // the list capacity for nb CTAs fits the resident wave
         nb = nb2;              // fewer CTAs per slot: longer lists, recheck
     }
+    if (Ge::PERW % 128) vp.ktma = 0;  // TMA destinations need 128-byte aligned stages
     vp.list_cap = (int)((cap_cells + nb - 1) / nb);
     if (!glist) vp.glist = nullptr;  // else: the caller's scratch of slots * (cap_cells + nb) entries
     const int cap = occ * sms;

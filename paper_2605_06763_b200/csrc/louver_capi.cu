@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "louver_aux.cuh"
 #include "louver_b200.h"
 #include "louver_threshold.cuh"
@@ -89,6 +91,10 @@ struct lv_ctx {
     int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     lvg::GroupIndex* gi = nullptr;  // the reference's grouped index (cfg.group_index)
+    int ktma = 0;                   // key blocks by TMA in the bf16 layer kernel (LV_KTMA=1; A/B: slower)
+    CUtensorMap kmap{};             // its tensor map, for kmap_K / kmap_cap
+    const void* kmap_K = nullptr;
+    long long kmap_cap = 0;
     std::mutex writer;
 };
 
@@ -161,6 +167,7 @@ void choose_splits(lv_ctx* c) {
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
         if (const char* e = std::getenv("LV_L2PF")) c->l2pf = std::atoi(e);
         if (const char* e = std::getenv("LV_PRE")) c->npre = std::min(3, std::max(0, std::atoi(e)));
+        if (const char* e = std::getenv("LV_KTMA")) c->ktma = std::atoi(e);
         c->nb = (int)std::min<long long>(nb, 4096);
     }
     // fp32 kernel (fp32 query and dense, brute force for both dtypes): chunks of kChunk keys
@@ -256,6 +263,33 @@ lvg::ArenaView arena_view(const lv_ctx* c) {
     return a;
 }
 
+// The K arena [slots * cap][DP] bf16 as a 2D tensor map: box 64 x 16 (one 128-byte column
+// half of a 16-key block), 128-byte swizzle — the layer kernel's stage layout.
+int ensure_kmap(lv_ctx* c) {
+    if (c->kmap_K == c->K && c->kmap_cap == c->cap) return LV_OK;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode) return fail(LV_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)c->DP, (cuuint64_t)c->slots * (cuuint64_t)c->cap};
+    const cuuint64_t strides[1] = {(cuuint64_t)c->DP * 2};
+    const cuuint32_t box[2] = {64, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&c->kmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->K, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LV_ERUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    c->kmap_K = c->K;
+    c->kmap_cap = c->cap;
+    return LV_OK;
+}
+
 int sync_if_host(int where, cudaStream_t st) {
     if (where == LV_HOST) LV_CUDA(cudaStreamSynchronize(st));
     return LV_OK;
@@ -304,6 +338,8 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         lp.p.tot_trace = c->trace;
         lp.l2pf = c->l2pf;
         lp.npre = c->npre;
+        lp.ktma = c->ktma && c->kmap_K == c->K;  // the map is encoded by lv_create / lv_reserve
+        if (lp.ktma) lp.kmap = c->kmap;
         // cells complete before the last insert enqueued ahead of this query: the insert kernel
         // that may still be draining under PDL writes only the cell of key n - 1
         lp.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
@@ -461,6 +497,11 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
             return cleanup("alloc grouped index", e);
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup("init", e);
+    if (cfg->dtype == LV_BF16 && c->ktma)
+        if (int rc = ensure_kmap(c)) {
+            lv_destroy(c);
+            return rc;
+        }
     *out = c;
     return LV_OK;
 }
@@ -586,6 +627,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->chunks_per_split = probe_geo.chunks_per_split;
     c->nb = probe_geo.nb;
     c->cfg.capacity = capacity;
+    if (c->cfg.dtype == LV_BF16 && c->ktma) return ensure_kmap(c);
     return LV_OK;
 }
 

@@ -33,6 +33,8 @@
 // cells are requested before griddepcontrol.wait.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "louver_common.cuh"
 #include "louver_kernels.cuh"
 
@@ -52,7 +54,17 @@ struct LayerParams {
     long long sealed;          // cells complete when the query was enqueued (immutable summaries)
     int npre;                  // summary sub-blocks requested before griddepcontrol.wait (0..3)
     int l2pf;                  // experiment: L2 bulk prefetch of surviving cells' keys from the probe
+    int ktma;                  // key blocks by TMA (kmap) instead of cp.async
+    alignas(64) CUtensorMap kmap;  // K arena as [slots * cap][DP] bf16, box 64 x 16, 128-byte swizzle
 };
+
+// one 2D TMA tile (box of the tensor map) into shared memory, completing on an mbarrier
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int x, int y, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
 
 // Ballot over pair lanes (lane = k G + g for row k of a 32/G-row block) ->
 // bit k set iff any head of row k is set.
@@ -114,7 +126,8 @@ struct C9 {
     static constexpr int OFF_Q = OFF_FRP + SZ_FRP;                    // [G][DP+4] f32
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
     static constexpr int MISC = 5 * G + 16 * G + 32;
-    static constexpr int FIX = (OFF_M + MISC * 4 + 127) / 128 * 128;
+    static constexpr int OFF_BAR = (OFF_M + MISC * 4 + 7) / 8 * 8;   // [16 warps][3 stages] mbarriers
+    static constexpr int FIX = (OFF_BAR + 16 * 3 * 8 + 127) / 128 * 128;
     static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
     static constexpr int BUDGET = 223 * 1024;    // + the survivor list, within 227 KB
     static constexpr int NW0 = (BUDGET - FIX) / PERW;
@@ -152,6 +165,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
     const unsigned ring = smem_u32(wbase);
     const int b7 = (int)((ring >> 7) & 7u);  // the same for every stage of the warp (4 KiB apart)
+    const bool ktma = vp.ktma != 0;
+    const unsigned kbar = smem_u32(smem + Ge::OFF_BAR) + warp * 24;  // this warp's 3 stage barriers
+    unsigned kph = 0;                                                // their phase bits
+    if (ktma) {
+        if (lane == 0) {
+            for (int i = 0; i < 3; ++i) mbar_init(kbar + 8 * i, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncwarp();
+    }
     float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
     const int q4 = lane & 3;
@@ -471,6 +494,20 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 doff[kk] = lay(row, c, b7);
             }
             auto k_issue = [&](int t, int kb, int stage) {  // rows past n land as zeros
+                if (ktma) {  // one TMA tile per 128-byte column half; rows past n are the arena's zeros
+                    if (t < ntask) {
+                        __syncwarp();
+                        if (lane == 0) {
+                            fence_proxy_async();  // the stage's last generic reads / cp.async writes
+                            const unsigned bar = kbar + 8 * stage, dst = ring + stage * Ge::STAGE;
+                            mbar_expect_tx(bar, Ge::STAGE);
+                            const int row = (int)(slot * p.cap) + kb;
+#pragma unroll
+                            for (int h = 0; h < DP / 64; ++h) tma_load_2d(dst + h * 2048, &vp.kmap, h * 64, row, bar);
+                        }
+                    }
+                    return;
+                }
                 if (t < ntask) {
                     const unsigned char* src = reinterpret_cast<const unsigned char*>(Ks) + (size_t)kb * RB + lane * 16;
                     const unsigned dst = ring + stage * Ge::STAGE;
@@ -504,7 +541,12 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (lane == 0 && tn < ntask) cb = atomicAdd(iscr + 3, 1);
                 const int kn = tn < ntask ? key0(tn) : 0;
                 k_issue(tn, kn, s1);
-                cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
+                if (ktma) {  // K(t) landed
+                    mbar_wait(kbar + 8 * st, (kph >> st) & 1u);
+                    kph ^= 1u << st;
+                } else {
+                    cpa_wait<2>();  // K(t) landed (V(t-1), K(t+1) may pend)
+                }
                 __syncwarp();
                 // -- scores: 16 keys x [q0|q1|q2] per head
                 const unsigned sb = ring + st * Ge::STAGE;
@@ -652,7 +694,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 }
                 cpa_commit();
                 // -- fold V(t-1) (frame m_{t-1}), then move o to frame m_t
-                cpa_wait<2>();  // V(t-1) landed (K(t+1), V(t) may pend)
+                if (ktma)
+                    cpa_wait<1>();  // V(t-1) landed (V(t) may pend)
+                else
+                    cpa_wait<2>();  // V(t-1) landed (K(t+1), V(t) may pend)
                 __syncwarp();
                 if (pend) {
                     const unsigned vb = ring + s2 * Ge::STAGE + v_off;

@@ -206,7 +206,11 @@ def run_decode_sim(keys, values, queries, cfg: DecodeSimConfig, prefill: int = 0
     totals = totals_d.cpu().numpy()
     taus = tau_d.cpu().numpy()[:, 0]
     rep = MetricsReport(steps=steps - prefill, flushes=layer.flush_count, violations=int(viol_d.item()))
-    g = 2.0 if cfg.build.enclosing == "aabb" else 1.0
+    # statistics of the device index: its groups are cells of cell_keys contiguous keys with
+    # one AABB each (gate cost 2 per cell), so gate_cost_equiv and the speed-up estimate
+    # use that geometry (bench.cpp:13-20 with g = 2, r = cell_keys), not cfg.build's r
+    g = 2.0
+    r_dev = max(1, int(layer.geometry().get("cell_keys", cfg.build.r)))
     inv = 1.0 / rep.steps if rep.steps else 0.0
     sum_speedup = 0.0
     for t in range(prefill, steps):
@@ -220,11 +224,11 @@ def run_decode_sim(keys, values, queries, cfg: DecodeSimConfig, prefill: int = 0
         rep.mean_f_scan += f_scan
         rep.mean_keys_scanned += scanned
         rep.mean_groups_tested += groups
-        rep.mean_gate_cost_equiv += 2.0 * groups / max(1, cfg.build.r)
+        rep.mean_gate_cost_equiv += g * groups / r_dev
         rep.mean_selected += float(counts[t, 0])
         rep.mean_retrieved += retrieved
         rep.mean_tau += float(taus[t]) if math.isfinite(float(taus[t])) else 0.0
-        sum_speedup += speedup_estimate(g, cfg.build.r, min(max(f_scan, 0.0), 1.0))
+        sum_speedup += speedup_estimate(g, r_dev, min(max(f_scan, 0.0), 1.0))
         if cfg.verify and n == 0 and counts[t, 0] != 0:
             rep.violations += 1
     for f in ("mean_f_scan", "mean_keys_scanned", "mean_groups_tested", "mean_gate_cost_equiv", "mean_selected",

@@ -76,6 +76,23 @@ def main():
             print(f"layer {l} merge body cycles: stage {d(18, 19):.0f}  heads {d(19, 20):.0f}  accumulate {d(20, 21):.0f}  "
                   f"write {d(21, 22):.0f}")
     print(f"per-layer period (end to end): {np.diff(ends).mean() / 1e3:.2f} us")
+    # merge body of the ticket winners: won -> partials staged (11) -> combined (14) -> end (7)
+    seg = []
+    for t in trs:
+        w = t[(t[:, 8] > 0) & (t[:, 11] > 0) & (t[:, 14] > 0)]
+        for r in w:
+            seg.append(((r[11] - r[8]) / 1e3, (r[14] - r[11]) / 1e3, (r[7] - r[14]) / 1e3))
+    if seg:
+        a = np.median(np.array(seg), axis=0)
+        print(f"merge (median over winners): stage partials {a[0]:.2f} us, headers + accumulate {a[1]:.2f} us, "
+              f"write {a[2]:.2f} us")
+    # CTA partial: the CTA's last warp done (5 is warp 0 only) -> partial written (6)
+    par = []
+    for t in trs:
+        w = t[(t[:, 5] > 0) & (t[:, 6] > 0)]
+        par.extend(((w[:, 6] - w[:, 5]) / 1e3).tolist())
+    if par:
+        print(f"warp 0 tasks done -> CTA partial written: median {np.median(par):.2f} us")
     # per slot (kv head): the team's survivor cells and when its last CTA finished its tasks
     nb = int(layers[0].geometry().get("team_ctas_per_slot", 18)) if hasattr(layers[0], "geometry") else 18
     for l in (1, 4):

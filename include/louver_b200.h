@@ -169,7 +169,10 @@ size_t lv_query_workspace_bytes(const lv_ctx* ctx);
  * one device->host copy of out, one synchronisation — the host-buffer form of the
  * decode step. staging: optional DEVICE scratch of lv_query_layers_staging_bytes()
  * bytes; NULL uses ctxs[0]'s internal staging (calls sharing ctxs[0] serialise).
- * Each layer's query uses its context's internal workspace. */
+ * Each layer's query uses its context's internal workspace. With pinned buffers, the
+ * internal staging and a non-default stream, the step runs as a CUDA graph captured on
+ * the first call and replayed while the contexts, buffers and stream stay the same
+ * (LV_LAYERS_GRAPH=0 disables it). */
 int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau, float scale, int strict,
                     float* out, void* staging, void* stream);
 size_t lv_query_layers_staging_bytes(const lv_ctx* ctx, int L);

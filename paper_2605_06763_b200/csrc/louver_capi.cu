@@ -4,6 +4,7 @@
 // louver_kernels.cuh / louver_aux.cuh.
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -87,6 +88,18 @@ struct lv_ctx {
     void* stage = nullptr;       // lv_query_layers' internal staging (lazily grown)
     size_t stage_bytes = 0;
     std::mutex stage_mu;
+    long long version = 0;       // unique per context and per arena (lv_reserve): cached graphs expire
+    // lv_query_layers' CUDA graph of one decode step (copy in, L queries, copy out), cached for
+    // the last (contexts, host buffers, staging, stream) it was called with
+    struct LayersGraph {
+        std::vector<const lv_ctx*> ctxs;
+        std::vector<long long> versions;
+        const void *q = nullptr, *tau = nullptr, *out = nullptr, *base = nullptr;
+        float scale = 0.0f;
+        int strict = 0;
+        cudaStream_t st = nullptr;
+        cudaGraphExec_t exec = nullptr;
+    } lgraph;
     int l2pf = 0;                // experiment knob (LV_L2PF)
     int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
@@ -252,6 +265,11 @@ int convert_into(lv_ctx* c, const void* src_dev, int src_dtype, void* arena, lon
                   : launch_convert<float, float>(c, src_dev, arena, n, first, st);
     if (!bf) return fail(LV_EINVAL, "bf16 source needs a bf16 cache");
     return launch_convert<__nv_bfloat16, __nv_bfloat16>(c, src_dev, arena, n, first, st);
+}
+
+long long next_version() {  // process-wide: a context reusing a freed one's address never matches
+    static std::atomic<long long> v{0};
+    return ++v;
 }
 
 lvg::ArenaView arena_view(const lv_ctx* c) {
@@ -461,6 +479,7 @@ int lv_create(const lv_config* cfg, lv_ctx** out) {
     c->r_log2 = ilog2(c->r);
     c->slots = cfg->batch * cfg->n_kv_heads;
     c->rows = c->slots * c->G;
+    c->version = next_version();
     c->cap = (cfg->capacity + kCapAlign - 1) / kCapAlign * kCapAlign;
     c->cap_cells = c->cap / c->r;
     c->bits_words = c->cap / 32;
@@ -516,6 +535,7 @@ int lv_destroy(lv_ctx* c) {
     cudaFree(c->ins_ticket);
     cudaFree(c->ws_mem);
     if (c->stage) cudaFree(c->stage);
+    if (c->lgraph.exec) cudaGraphExecDestroy(c->lgraph.exec);
     if (c->gi) {
         lvg::destroy(*c->gi);
         delete c->gi;
@@ -627,6 +647,7 @@ int lv_reserve(lv_ctx* c, int64_t capacity, void* stream) {
     c->chunks_per_split = probe_geo.chunks_per_split;
     c->nb = probe_geo.nb;
     c->cfg.capacity = capacity;
+    c->version = next_version();
     if (c->cfg.dtype == LV_BF16 && c->ktma) return ensure_kmap(c);
     return LV_OK;
 }
@@ -830,21 +851,74 @@ int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau
     float* od = reinterpret_cast<float*>(base + align256(sizeof(float) * L * rows * d));
     float* td = reinterpret_cast<float*>(base + 2 * align256(sizeof(float) * L * rows * d));
     // one copy in for every layer's q and tau, the L queries back to back, one copy out
-    LV_CUDA(cudaMemcpyAsync(qd, q, sizeof(float) * L * rows * d, cudaMemcpyHostToDevice, st));
-    LV_CUDA(cudaMemcpyAsync(td, tau, sizeof(float) * L * rows, cudaMemcpyHostToDevice, st));
-    for (int l = 0; l < L; ++l) {
-        lv_query_args a{};
-        a.q = qd + (size_t)l * rows * d;
-        a.tau = td + (size_t)l * rows;
-        a.scale = scale;
-        a.algo = LV_ALGO_TA;
-        a.strict = strict;
-        a.where = LV_DEVICE;
-        a.out = od + (size_t)l * rows * d;
-        a.stream = stream;
-        if (int rc = lv_query(ctxs[l], &a)) return rc;
+    auto enqueue = [&]() -> int {
+        LV_CUDA(cudaMemcpyAsync(qd, q, sizeof(float) * L * rows * d, cudaMemcpyHostToDevice, st));
+        LV_CUDA(cudaMemcpyAsync(td, tau, sizeof(float) * L * rows, cudaMemcpyHostToDevice, st));
+        for (int l = 0; l < L; ++l) {
+            lv_query_args a{};
+            a.q = qd + (size_t)l * rows * d;
+            a.tau = td + (size_t)l * rows;
+            a.scale = scale;
+            a.algo = LV_ALGO_TA;
+            a.strict = strict;
+            a.where = LV_DEVICE;
+            a.out = od + (size_t)l * rows * d;
+            a.stream = stream;
+            if (int rc = lv_query(ctxs[l], &a)) return rc;
+        }
+        LV_CUDA(cudaMemcpyAsync(out, od, sizeof(float) * L * rows * d, cudaMemcpyDeviceToHost, st));
+        return LV_OK;
+    };
+    // The step as a CUDA graph (one launch instead of 2 + L + 1, kernels scheduled back to back)
+    // when it can be captured: a non-default stream that is not itself capturing, page-locked
+    // host buffers, the context-internal staging (its lock serialises the calls).
+    bool graph = lock.owns_lock() && st != nullptr;
+    if (graph) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        graph = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+        for (const void* h : {(const void*)q, (const void*)tau, (const void*)out}) {
+            cudaPointerAttributes pa{};
+            graph = graph && cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        }
+        cudaGetLastError();
+        if (const char* e = std::getenv("LV_LAYERS_GRAPH")) graph = graph && std::atoi(e) != 0;
     }
-    LV_CUDA(cudaMemcpyAsync(out, od, sizeof(float) * L * rows * d, cudaMemcpyDeviceToHost, st));
+    if (!graph) {
+        if (int rc = enqueue()) return rc;
+        LV_CUDA(cudaStreamSynchronize(st));
+        return LV_OK;
+    }
+    auto& g = c0->lgraph;
+    bool hit = g.exec && g.q == q && g.tau == tau && g.out == out && g.base == base && g.scale == scale &&
+               g.strict == strict && g.st == st && (int)g.ctxs.size() == L;
+    for (int l = 0; hit && l < L; ++l) hit = g.ctxs[l] == ctxs[l] && g.versions[l] == ctxs[l]->version;
+    if (!hit) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        LV_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue();
+        cudaGraph_t gr = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(st, &gr);
+        if (rc) {
+            if (gr) cudaGraphDestroy(gr);
+            return rc;
+        }
+        if (e != cudaSuccess) return fail(LV_ERUNTIME, std::string("lv_query_layers capture: ") + cudaGetErrorString(e));
+        const cudaError_t ei = cudaGraphInstantiate(&g.exec, gr, 0);
+        cudaGraphDestroy(gr);
+        if (ei != cudaSuccess) return fail(LV_ERUNTIME, std::string("lv_query_layers graph: ") + cudaGetErrorString(ei));
+        g.ctxs.assign(ctxs, ctxs + L);
+        g.versions.resize(L);
+        for (int l = 0; l < L; ++l) g.versions[l] = ctxs[l]->version;
+        g.q = q;
+        g.tau = tau;
+        g.out = out;
+        g.base = base;
+        g.scale = scale;
+        g.strict = strict;
+        g.st = st;
+    }
+    LV_CUDA(cudaGraphLaunch(g.exec, st));
     LV_CUDA(cudaStreamSynchronize(st));
     return LV_OK;
 }

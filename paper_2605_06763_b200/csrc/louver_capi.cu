@@ -688,6 +688,7 @@ int lv_build(lv_ctx* c, const void* K, const void* V, int64_t n, int src_dtype, 
     Counters h{n, n, 0, 0};
     LV_CUDA(cudaMemcpyAsync(c->ctr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
     LV_CUDA(cudaStreamSynchronize(st));
+    c->version = next_version();  // a rebuild may shrink n: captured launch parameters expire
     c->n = n;
     c->indexed = n;
     c->flushes = 0;

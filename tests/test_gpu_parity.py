@@ -132,6 +132,55 @@ def test_query_layers_host_equals_device_queries(torch):
         query_layers_host(layers, q[:, :, :4], t, out)
 
 
+def test_query_layers_graph_follows_inputs_inserts_and_growth(torch):
+    """lv_query_layers replays a cached CUDA graph when its buffers are pinned and the stream
+    is not the default one: new q contents, keys pushed between steps and an arena that grew
+    (lv_reserve) must all be reflected, exactly as per-layer device queries see them."""
+    from paper_2605_06763_b200 import query_layers_host
+
+    L, H, G, d, n = 2, 2, 4, 128, 2000
+    layers = []
+    for l in range(L):
+        K = np.stack([synth.keys(n, d, 700 + 10 * l + h) for h in range(H)])[None]
+        V = np.stack([synth.keys(n, d, 750 + 10 * l + h) for h in range(H)])[None]
+        ly = LouverLayer(d, H, G, 1, n + 64, BuildConfig(S=1, r=16, grouping="contiguous", enclosing="aabb"),
+                         buffer_capacity=16)
+        ly.build(K, V)
+        layers.append(ly)
+    qh = torch.zeros((L, 1, H * G, d), dtype=torch.float32).pin_memory()
+    th = torch.full((L, 1, H * G), 30.0, dtype=torch.float32).pin_memory()
+    oh = torch.zeros((L, 1, H * G, d), dtype=torch.float32).pin_memory()
+    stream = torch.cuda.Stream()
+    rng = np.random.default_rng(3)
+
+    def step_and_check(tag):
+        qh.copy_(torch.from_numpy(rng.standard_normal((L, 1, H * G, d)).astype(np.float32)) * 2.0)
+        query_layers_host(layers, qh.numpy(), th.numpy(), oh.numpy(), stream=stream.cuda_stream)
+        for l in range(L):
+            want = torch.zeros((1, H * G, d), device="cuda")
+            layers[l].query_device(qh[l].cuda(), th[l].cuda(), want)
+            torch.cuda.synchronize()
+            np.testing.assert_allclose(oh[l].numpy(), want.cpu().numpy(), rtol=1e-6, atol=1e-6, err_msg=f"{tag} {l}")
+
+    step_and_check("first")
+    step_and_check("replay")  # same buffers: the cached graph, new q contents
+    for j in range(40):  # inserts across a flush (B = 16) between steps
+        for ly in layers:
+            k = torch.from_numpy(rng.standard_normal((1, H, d)).astype(np.float32) * 3.0).cuda()
+            ly.push_key(k, k)
+    step_and_check("after inserts")
+    for j in range(64):  # past the arena capacity: lv_reserve moves the arrays
+        for ly in layers:
+            if ly.n >= ly._ctx.cfg.capacity:
+                from paper_2605_06763_b200._capi import check
+                new_cap = 2 * ly._ctx.cfg.capacity
+                check(ly._ctx.lib.lv_reserve(ly._ctx.h, new_cap, None), "lv_reserve")
+                ly._ctx.cfg.capacity = new_cap
+            k = torch.from_numpy(rng.standard_normal((1, H, d)).astype(np.float32)).cuda()
+            ly.push_key(k, k)
+    step_and_check("after growth")
+
+
 def test_strict_toggle(torch):  # test_cache.cpp:123-144
     c = LouverCache(4, BuildConfig(S=2, r=2), 64)
     keys = np.array([[1, 1, 1, 1], [-1, -1, -1, -1], [2, 2, 2, 2]], np.float32)

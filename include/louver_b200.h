@@ -344,6 +344,10 @@ int lv_step_store(const int64_t* step, const void* src, void* dst, int64_t strid
 int lv_step_reservoir(const int64_t* step, const int32_t* slot_of_step, int64_t row0, uint32_t* ids, int nslots,
                       int64_t ld, void* stream);
 int lv_step_advance(int64_t* step, void* stream);
+/* The end of a decode step in one launch: the copies (as lv_step_copies), the reservoir
+ * write (as lv_step_reservoir; ids may be NULL), then the step counter's advance. */
+int lv_step_epilogue(int64_t* step, const lv_step_copy* copies, int ncopies, const int32_t* slot_of_step,
+                     int64_t row0, uint32_t* ids, int nslots, int64_t ld, void* stream);
 
 /* --- Snapshots (io.hpp:40-51, io.cpp:205-317) --------------------------------
  * "LVKD" dataset: magic, version 1, n, d (u32 LE), n*d f32 row-major. With

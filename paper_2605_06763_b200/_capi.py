@@ -143,6 +143,7 @@ _SIGS = {
     "lv_step_store": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
     "lv_step_reservoir": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int, C.c_int64, _P]),
     "lv_step_advance": (C.c_int, [_P, _P]),
+    "lv_step_epilogue": (C.c_int, [_P, _P, C.c_int, _P, C.c_int64, _P, C.c_int, C.c_int64, _P]),
     "lv_group_candidates": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_int, _P, _P, C.c_int64,
                                       C.POINTER(C.c_int64), C.POINTER(lv_group_stats), _P]),
     "lv_group_thresholds": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, _P]),

@@ -1321,6 +1321,24 @@ int lv_step_reservoir(const int64_t* step, const int32_t* slot_of_step, int64_t 
     return LV_OK;
 }
 
+int lv_step_epilogue(int64_t* step, const lv_step_copy* copies, int ncopies, const int32_t* slot_of_step,
+                     int64_t row0, uint32_t* ids, int nslots, int64_t ld, void* stream) {
+    if (!step || ncopies < 0 || ncopies > 8 || (ncopies && !copies) || (ids && (!slot_of_step || row0 < 0 || nslots < 1 || ld < 0)))
+        return fail(LV_EINVAL, "lv_step_epilogue: bad arguments");
+    lvkt::StepCopies cs{};
+    for (int i = 0; i < ncopies; ++i) {
+        const lv_step_copy& c = copies[i];
+        if (!c.src || !c.dst || c.stride < 0 || c.bytes < 0 || c.bytes % 4 || c.stride % 4 || (c.dir != 0 && c.dir != 1))
+            return fail(LV_EINVAL, "lv_step_epilogue: bad copy (4-byte multiples, dir 0 or 1)");
+        cs.c[i] = {(const uint32_t*)c.src, (uint32_t*)c.dst, c.stride / 4, c.bytes / 4, c.dir};
+    }
+    cs.n = ncopies;
+    lvkt::step_epilogue_kernel<<<1, 256, 0, S(stream)>>>(reinterpret_cast<long long*>(step), cs, slot_of_step, row0,
+                                                         ids, nslots, ld);
+    LV_CUDA(cudaGetLastError());
+    return LV_OK;
+}
+
 int lv_step_advance(int64_t* step, void* stream) {
     if (!step) return fail(LV_EINVAL, "lv_step_advance: null step");
     lvkt::step_advance_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<long long*>(step));

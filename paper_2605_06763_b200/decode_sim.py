@@ -349,8 +349,7 @@ def run_decode_graph(keys, values, queries, H_kv: int, G: int, cfg: DecodeSimCon
         check(lib.lv_step_copies(sp, loads, 3, st), "lv_step_copies")
         if oracle is not None:
             estimate_tau_layer(layer, ids_d, cap, q_buf, oracle, tau_buf, stream=st)
-        counts.zero_()
-        if verify:
+        if verify:  # (lv_query zeroes counts itself)
             bits.zero_()
         layer.query_device(q_buf, tau_buf, out_buf, strict=cfg.strict_threshold, counts=counts, sel_bits=bits,
                            stream=st)
@@ -359,10 +358,10 @@ def run_decode_graph(keys, values, queries, H_kv: int, G: int, cfg: DecodeSimCon
                                            ref_bits.data_ptr(), st), "lv_brute_force_range")
             check(lib.lv_bits_diff(bits.data_ptr(), ref_bits.data_ptr(), words, rq, viol.data_ptr(), st),
                   "lv_bits_diff")
-        check(lib.lv_step_copies(sp, stores, 2, st), "lv_step_copies")
         layer.push_key(k_buf, v_buf, stream=st)
-        check(lib.lv_step_reservoir(sp, slot_d.data_ptr(), 0, ids_d.data_ptr(), slots, cap, st), "lv_step_reservoir")
-        check(lib.lv_step_advance(sp, st), "lv_step_advance")
+        # the step's log, the reservoir's write for row t and the counter advance: one launch
+        check(lib.lv_step_epilogue(sp, stores, 2, slot_d.data_ptr(), 0, ids_d.data_ptr(), slots, cap, st),
+              "lv_step_epilogue")
 
     stream = torch.cuda.Stream()
     graph = torch.cuda.CUDAGraph()

@@ -217,4 +217,25 @@ __global__ void step_reservoir_kernel(const long long* __restrict__ step, const 
 
 __global__ void step_advance_kernel(long long* step) { *step += 1; }
 
+// The end of a decode step in one launch (one block): the step's log stores, the
+// reservoir's write for the step's row, then the counter advance (after every read of it)
+__global__ void step_epilogue_kernel(long long* step, const __grid_constant__ StepCopies cs,
+                                     const int* __restrict__ slot_of_step, long long row0, uint32_t* __restrict__ ids,
+                                     int nslots, long long ld) {
+    const long long t = *step;
+    for (int k = 0; k < cs.n; ++k) {
+        const StepCopy& c = cs.c[k];
+        const long long off = t * c.stride_words;
+        const uint32_t* s = c.dir == 0 ? c.src + off : c.src;
+        uint32_t* d = c.dir == 0 ? c.dst : c.dst + off;
+        for (long long i = threadIdx.x; i < c.words; i += blockDim.x) d[i] = s[i];
+    }
+    if (ids) {
+        const int slot = slot_of_step[t];
+        for (int i = threadIdx.x; slot >= 0 && i < nslots; i += blockDim.x) ids[i * ld + slot] = (uint32_t)(row0 + t);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *step = t + 1;
+}
+
 }  // namespace lvkt

@@ -181,3 +181,43 @@ def test_snapshot_bytes_equal_reference_and_load(S, r, grouping, enclosure, seed
         assert load_index(dev2, pr) == ref.indexed_count()
         check_index(dev2, ref, d, S, enclosure)
         check_queries(dev2, ref, K, d, S, 2)
+
+
+@pytest.mark.parametrize("S,r,grouping,enclosure,n,d", [
+    (1, 1, "pca_tree", "ball", 37, 8),        # every key its own group
+    (8, 2, "pca_tree", "span_ball", 19, 8),   # S = d: one coordinate per subspace
+    (3, 64, "pca_tree", "aabb", 50, 10),      # one group holds every key (m < r)
+    (2, 5, "interleaved", "aabb", 23, 7),
+    (5, 3, "random", "span_ball", 41, 13),
+])
+def test_grouped_index_edge_shapes(S, r, grouping, enclosure, n, d):
+    """Degenerate shapes of index.cpp: r = 1, r > m, S = d, odd widths; the prefill build and
+    one appended block (push_key up to a flush) equal the reference's."""
+    K, V = keys_of("iid", n + 9, d, 31)
+    cfg = BuildConfig(S=S, r=r, grouping=grouping, enclosing=enclosure, rng_seed=11)
+    dev = LouverCache.adopt(K[:n], V[:n], cfg, 9)
+    ref = REF.Cache(d, REF.cfg(S, r, grouping, enclosure, 11), 9, K[:n], V[:n])
+    check_index(dev, ref, d, S, enclosure)
+    for j in range(n, n + 9):
+        dev.push_key(K[j], V[j])
+        ref.push_key(K[j], V[j])
+    assert dev.indexed_count() == ref.indexed_count() == n + 9
+    check_index(dev, ref, d, S, enclosure)
+    check_queries(dev, ref, K, d, S, 4)
+
+
+def test_grouped_index_errors():
+    """The reference's argument errors (query.cpp:84-87) and the API's own."""
+    d = 16
+    K, V = keys_of("iid", 64, d, 2)
+    dev = LouverCache.adopt(K, V, BuildConfig(S=4, r=4), 16)
+    q = K[0]
+    with pytest.raises(ValueError, match="tau_subspace required"):
+        query_full_subspace(dev, QueryRequest(q=q, tau=0.0))
+    with pytest.raises(ValueError, match="length != S"):
+        query_full_subspace(dev, QueryRequest(q=q, tau=0.0, tau_subspace=[0.0, 0.0]))
+    with pytest.raises(ValueError):
+        query_ta(dev, QueryRequest(q=q[:8], tau=0.0))
+    plain = LouverCache.adopt(K, V, BuildConfig(S=4, r=4), 16, group_index=False)
+    with pytest.raises(ValueError, match="grouped index"):
+        query_ta(plain, QueryRequest(q=q, tau=0.0))

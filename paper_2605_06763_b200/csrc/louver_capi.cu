@@ -100,7 +100,6 @@ struct lv_ctx {
         cudaStream_t st = nullptr;
         cudaGraphExec_t exec = nullptr;
     } lgraph;
-    int l2pf = 0;                // experiment knob (LV_L2PF)
     int npre = 3;                // experiment knob (LV_PRE)
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     lvg::GroupIndex* gi = nullptr;  // the reference's grouped index (cfg.group_index)
@@ -178,7 +177,6 @@ void choose_splits(lv_ctx* c) {
         // the resident wave (inst_v9.cu)
         long long nb = std::max(1LL, ((long long)c->sms + c->slots - 1) / c->slots);
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
-        if (const char* e = std::getenv("LV_L2PF")) c->l2pf = std::atoi(e);
         if (const char* e = std::getenv("LV_PRE")) c->npre = std::min(3, std::max(0, std::atoi(e)));
         if (const char* e = std::getenv("LV_KTMA")) c->ktma = std::atoi(e);
         c->nb = (int)std::min<long long>(nb, 4096);
@@ -354,7 +352,6 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         lp.nb = c->nb;
         lp.glist = w.glist;
         lp.p.tot_trace = c->trace;
-        lp.l2pf = c->l2pf;
         lp.npre = c->npre;
         lp.ktma = c->ktma && c->kmap_K == c->K;  // the map is encoded by lv_create / lv_reserve
         if (lp.ktma) lp.kmap = c->kmap;

@@ -53,7 +53,6 @@ struct LayerParams {
     int list_cap;              // entries per CTA list
     long long sealed;          // cells complete when the query was enqueued (immutable summaries)
     int npre;                  // summary sub-blocks requested before griddepcontrol.wait (0..3)
-    int l2pf;                  // experiment: L2 bulk prefetch of surviving cells' keys from the probe
     int ktma;                  // key blocks by TMA (kmap) instead of cp.async
     alignas(64) CUtensorMap kmap;  // K arena as [slots * cap][DP] bf16, box 64 x 16, 128-byte swizzle
 };
@@ -418,8 +417,6 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         }
                         scan = (int)((ce < n ? ce : n) - cs);
                     }
-                    if (gm && vp.l2pf)  // the cell's keys stream into L2 now; the exact phase finds them there
-                        bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(Ks) + ((size_t)cell << rl) * RB, (unsigned)(r * RB));
                     const unsigned m = __ballot_sync(0xffffffffu, gm != 0) & 0xffffu;
                     if (m) {  // append the survivors to the CTA's list
                         int base = 0;

@@ -20,6 +20,7 @@
 #include "louver_b200.h"
 #include "louver_threshold.cuh"
 #include "louver_dispatch.h"
+#include "louver_f32.cuh"
 #include "louver_groups.h"
 #include "louver_launch.h"
 #include "louver_v9.cuh"
@@ -104,6 +105,7 @@ struct lv_ctx {
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     lvg::GroupIndex* gi = nullptr;  // the reference's grouped index (cfg.group_index)
     int ktma = 0;                   // key blocks by TMA in the bf16 layer kernel (LV_KTMA=1; A/B: slower)
+    int f32_layer = 1;               // fp32 queries on the fused fp32 layer kernel (LV_F32_LAYER=0: round-1 kernel)
     CUtensorMap kmap{};             // its tensor map, for kmap_K / kmap_cap
     const void* kmap_K = nullptr;
     long long kmap_cap = 0;
@@ -172,13 +174,18 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 void choose_splits(lv_ctx* c) {
     c->sms = lvl::device_sms();
-    if (c->cfg.dtype == LV_BF16) {
-        // fused layer kernel: up to one CTA per SM per slot; the launch clamps the team to
-        // the resident wave (inst_v9.cu)
+    {
+        // fused layer kernels (bf16 and fp32): up to one CTA per SM per slot; the launch
+        // clamps the team to the resident wave (inst_v9.cu, inst_f32.cu)
+        // ... and no more CTAs than 64-cell shares of the arena: a small slot (C1: 2048
+        // cells) spread over every SM leaves each CTA a handful of cells and a long merge
+        // (C1 fp32: 148 CTAs 17.5 us, 32 CTAs 13.1 us)
         long long nb = std::max(1LL, ((long long)c->sms + c->slots - 1) / c->slots);
+        nb = std::max(1LL, std::min(nb, (c->cap_cells + 63) / 64));
         if (const char* e = std::getenv("LV_NB")) nb = std::max(1LL, std::atoll(e));
         if (const char* e = std::getenv("LV_PRE")) c->npre = std::min(3, std::max(0, std::atoi(e)));
         if (const char* e = std::getenv("LV_KTMA")) c->ktma = std::atoi(e);
+        if (const char* e = std::getenv("LV_F32_LAYER")) c->f32_layer = std::atoi(e);
         c->nb = (int)std::min<long long>(nb, 4096);
     }
     // fp32 kernel (fp32 query and dense, brute force for both dtypes): chunks of kChunk keys
@@ -359,6 +366,16 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         // that may still be draining under PDL writes only the cell of key n - 1
         lp.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
         e = lvk9::launch_layer_v9(c->DP, c->G, mode == lvk::kDense, lp, c->slots, c->sms, st, c->layer_geo);
+    } else if (mode == lvk::kQuery && c->f32_layer && (c->DP == 128 || c->DP == 256)) {
+        // fp32 caches: the fused fp32 layer kernel (normative dots on the CUDA cores)
+        lvkf::F32Params fp{};
+        fp.p = p;
+        fp.sum = reinterpret_cast<const float*>(c->lo);
+        fp.stickets = w.stickets;
+        fp.nb = c->nb;
+        fp.glist = w.glist;
+        fp.sealed = c->n > 0 ? (c->n - 1) >> c->r_log2 : 0;
+        e = lvkf::launch_layer_f32(c->DP, c->G, fp, c->slots, c->sms, st, c->layer_geo);
     } else {
         e = lvk::launch_query(c->cfg.dtype, c->DP, c->G, mode, p, grid, st);
     }

@@ -127,7 +127,10 @@ def test_query_layers_host_equals_device_queries(torch):
         want = torch.zeros((1, H * G, d), device="cuda")
         layers[l].query_device(torch.from_numpy(qs[l]).cuda(), torch.from_numpy(ts[l]).cuda(), want)
         torch.cuda.synchronize()
-        assert np.array_equal(out[l], want.cpu().numpy()), l
+        # same inputs, same kernel: equal up to the fp32 summation order, which the warps'
+        # dynamic task claiming may change from launch to launch
+        w = want.cpu().numpy()
+        assert np.abs(out[l] - w).max() <= 1e-5 * np.abs(w).max(), l
     with pytest.raises(ValueError):
         query_layers_host(layers, q[:, :, :4], t, out)
 
@@ -155,12 +158,16 @@ def test_query_layers_graph_follows_inputs_inserts_and_growth(torch):
 
     def step_and_check(tag):
         qh.copy_(torch.from_numpy(rng.standard_normal((L, 1, H * G, d)).astype(np.float32)) * 2.0)
+        stream.wait_stream(torch.cuda.current_stream())  # the inserts were enqueued on the current stream
         query_layers_host(layers, qh.numpy(), th.numpy(), oh.numpy(), stream=stream.cuda_stream)
         for l in range(L):
             want = torch.zeros((1, H * G, d), device="cuda")
             layers[l].query_device(qh[l].cuda(), th[l].cuda(), want)
             torch.cuda.synchronize()
-            np.testing.assert_allclose(oh[l].numpy(), want.cpu().numpy(), rtol=1e-6, atol=1e-6, err_msg=f"{tag} {l}")
+            # equal up to the fp32 summation order (relative to the output's scale: the
+            # warps' dynamic task claiming may change the order from launch to launch)
+            w = want.cpu().numpy()
+            assert np.abs(oh[l].numpy() - w).max() <= 1e-5 * np.abs(w).max(), (tag, l)
 
     step_and_check("first")
     step_and_check("replay")  # same buffers: the cached graph, new q contents

@@ -50,6 +50,10 @@ CONFIGS = {
                workload="C2 Llama-3-8B-shaped decode layer (32 q / 8 kv heads, d=128), 128K ctx, batch 1, bf16 KV"),
     "c3": dict(batch=16, H_kv=8, G=4, d=128, n=32768, dtype="bf16", layers=2,
                workload="C3 same shape, batch 16 at 32K ctx, GQA-grouped probing"),
+    # C5's 1M-token context on ONE GPU (the unsharded point of the 2/4/8-GPU curve: with
+    # --gpus P under torchrun each rank holds n / P of it)
+    "c5": dict(batch=1, H_kv=8, G=4, d=128, n=1048576, dtype="bf16", layers=2,
+               workload="C5 1M-token context, C2 head shape, one GPU (unsharded)"),
 }
 SELECTIVITY = 0.05
 CELL = 16

@@ -621,6 +621,7 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (kern_us * 1e-6) / 1e9
     kname = (f"louver_layer_v9<{geo['dp']},{G}>" if cfg["dtype"] == "bf16"
+             else f"louver_layer_f32<{geo['dp']},{G}>" if geo["dp"] >= 128
              else f"louver_query_kernel<f32,{geo['dp']},{G},kQuery>")
     traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from a committed ncu capture
     try:

@@ -509,7 +509,7 @@ class LouverLayer:
         keys = ("dp", "cell_keys", "arena_rows", "cells", "splits", "chunks_per_split", "chunk_keys",
                 "smem_bytes")
         out = {k: int(v) for k, v in zip(keys, g)}
-        if self.dtype == LV_BF16:  # the fused layer kernel's launch geometry (after a query)
+        if self.dtype == LV_BF16 or self.d > 64:  # the fused layer kernel's launch geometry (after a query)
             lg = np.zeros((4,), np.int64)
             check(self._ctx.lib.lv_layer_geometry(self._ctx.h, lg.ctypes.data), "lv_layer_geometry")
             out.update(zip(("team_ctas_per_slot", "ctas_per_sm", "threads_per_cta", "layer_smem_bytes"),

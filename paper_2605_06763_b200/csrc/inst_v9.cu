@@ -4,10 +4,10 @@
 
 namespace lvk9 {
 
-template <int DP, int G, bool DENSE>
+template <int DP, int G, bool DENSE, bool CNT>
 static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st, int* geo) {
     using Ge = C9<DP, G>;
-    const void* fn = reinterpret_cast<const void*>(louver_layer_v9<DP, G, DENSE>);
+    const void* fn = reinterpret_cast<const void*>(louver_layer_v9<DP, G, DENSE, CNT>);
     // One resident wave, a slot's team CTAs side by side. CTA b of a team owns cells b,
     // b + nb, ...: its survivor list holds at most ceil(cap_cells / nb) u16 entries, in
     // shared memory when that fits, else in global scratch (the dense scan keeps no list).
@@ -58,20 +58,26 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE>, vp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE, CNT>, vp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 cudaError_t launch_layer_v9(int DP, int G, bool dense, LayerParams vp, int slots, int sms, cudaStream_t st,
                             int* geo) {
-#define LV9_G(D)                                                                                       \
-    switch (G) {                                                                                       \
-        case 1: return dense ? launch_t<D, 1, true>(vp, slots, sms, st, geo) : launch_t<D, 1, false>(vp, slots, sms, st, geo); \
-        case 2: return dense ? launch_t<D, 2, true>(vp, slots, sms, st, geo) : launch_t<D, 2, false>(vp, slots, sms, st, geo); \
-        case 4: return dense ? launch_t<D, 4, true>(vp, slots, sms, st, geo) : launch_t<D, 4, false>(vp, slots, sms, st, geo); \
-        case 8: return dense ? launch_t<D, 8, true>(vp, slots, sms, st, geo) : launch_t<D, 8, false>(vp, slots, sms, st, geo); \
-    }                                                                                                  \
+    // dense decode never reports counts; a query does when p.counts is set
+    const int mode = dense ? 0 : (vp.p.counts ? 2 : 1);
+#define LV9_M(D, GG)                                                                                   \
+    return mode == 0 ? launch_t<D, GG, true, false>(vp, slots, sms, st, geo)                          \
+                     : (mode == 1 ? launch_t<D, GG, false, false>(vp, slots, sms, st, geo)            \
+                                  : launch_t<D, GG, false, true>(vp, slots, sms, st, geo));
+#define LV9_G(D)          \
+    switch (G) {          \
+        case 1: LV9_M(D, 1) \
+        case 2: LV9_M(D, 2) \
+        case 4: LV9_M(D, 4) \
+        case 8: LV9_M(D, 8) \
+    }                     \
     break;
     switch (DP) {
         case 64: LV9_G(64)
@@ -79,6 +85,7 @@ cudaError_t launch_layer_v9(int DP, int G, bool dense, LayerParams vp, int slots
         case 256: LV9_G(256)
     }
 #undef LV9_G
+#undef LV9_M
     return cudaErrorInvalidValue;
 }
 

@@ -127,7 +127,8 @@ size_t carve(const lv_ctx* c, unsigned char* base, Workspace* w) {
     const size_t rows = (size_t)c->rows;
     unsigned char* t = take(sizeof(int) * c->slots);
     const size_t nparts = (size_t)std::max(c->splits, c->nb);
-    unsigned char* part = take(sizeof(float) * c->slots * nparts * c->G * (c->DP + 2));
+    // partials: [slots][parts][G][DP+2] (+ the bf16 layer kernel's per-CTA counts [G][4])
+    unsigned char* part = take(sizeof(float) * c->slots * nparts * c->G * (c->DP + 6));
     unsigned char* q = take(sizeof(float) * rows * c->DP);
     unsigned char* o = take(sizeof(float) * rows * c->DP);
     unsigned char* tau = take(sizeof(float) * rows);
@@ -805,7 +806,9 @@ int lv_query(lv_ctx* c, const lv_query_args* a) {
     float* outd = direct ? a->out : (a->out ? w.out : nullptr);
     float* pod = (a->partial && direct) ? a->partial : (a->partial ? w.part_out : nullptr);
     int* cntd = a->counts ? (a->where == LV_DEVICE ? a->counts : w.counts) : nullptr;
-    if (cntd) LV_CUDA(cudaMemsetAsync(cntd, 0, sizeof(int) * c->rows * 4, st));
+    // the bf16 layer kernel writes every count itself (its merge sums the team's); the fp32
+    // kernels accumulate into zeroed counts
+    if (cntd && c->cfg.dtype != LV_BF16) LV_CUDA(cudaMemsetAsync(cntd, 0, sizeof(int) * c->rows * 4, st));
     if (a->totals) LV_CUDA(cudaMemsetAsync(a->totals, 0, sizeof(uint64_t) * 4, st));
     if (a->sel_bits)
         LV_CUDA(cudaMemsetAsync(a->sel_bits, 0, sizeof(uint32_t) * c->rows * c->bits_words, st));

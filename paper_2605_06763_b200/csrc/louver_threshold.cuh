@@ -50,6 +50,10 @@ __global__ void estimate_tau_kernel(const T* __restrict__ K, long long cap, int 
                                     const uint32_t* __restrict__ ids, long long ld, int cnt,
                                     const float* __restrict__ q, int mode, int pick, int np2,
                                     float* __restrict__ tau) {
+    // The kernel after this one (the layer query, launched with programmatic stream
+    // serialisation) may be dispatched onto the SMs this small grid leaves idle and start its
+    // pre-wait prologue now; it reads tau only after its griddepcontrol.wait.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     extern __shared__ __align__(16) float sh[];
     constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte vector
     const int vpr = DP / EPV, rstride = vpr + 1;  // vectors per row, staged row stride (padded)

@@ -124,7 +124,7 @@ struct C9 {
     static constexpr int OFF_FRP = OFF_FRE + SZ_FRE;
     static constexpr int OFF_Q = OFF_FRP + SZ_FRP;                    // [G][DP+4] f32
     static constexpr int OFF_M = OFF_Q + G * (DP + 4) * 4;            // misc
-    static constexpr int MISC = 5 * G + 16 * G + 32;
+    static constexpr int MISC = 5 * G + 16 * G + 32 + 4 * G;  // ..., iscr, per-head counts
     static constexpr int OFF_BAR = (OFF_M + MISC * 4 + 7) / 8 * 8;   // [16 warps][3 stages] mbarriers
     static constexpr int FIX = (OFF_BAR + 16 * 3 * 8 + 127) / 128 * 128;
     static constexpr int PERW = 3 * STAGE + 16 * CT * 4 + 16 * G * 4;  // ring, C tile, P
@@ -138,7 +138,9 @@ struct C9 {
     static_assert(NW >= 2, "Louver v9: shared memory budget too small");
 };
 
-template <int DP, int G, bool DENSE>
+// CNT: the launch writes p.counts (an instantiation of its own, so that the launches
+// without statistics — the bench, the production decode step — keep their code)
+template <int DP, int G, bool DENSE, bool CNT>
 __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ LayerParams vp) {
     using Ge = C9<DP, G>;
     constexpr bool PACK = G <= 4;  // P.V: hi and lo parts of P share one n-tile
@@ -156,6 +158,9 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     float* S_s = misc + 3 * G;         // [G]
     float* red = misc + 5 * G;         // [16 G]
     int* iscr = reinterpret_cast<int*>(misc + 21 * G);  // [32]
+    // iscr[32 .. 32 + 4 G): this CTA's per-head counts (selected, attended, keys scanned); they
+    // travel in its partial record and the merge writes the totals, so p.counts needs no
+    // zeroing before the launch
     // this CTA's surviving cells as interleave indices k (cell = blk + k nb): in smem, or in
     // global scratch when the list outgrows shared memory
     unsigned short* slist_s = reinterpret_cast<unsigned short*>(smem + Ge::DYN);
@@ -216,6 +221,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             iscr[2] = 0;  // survivors listed
             iscr[3] = 0;  // tasks claimed
         }
+        if (CNT && tid < 4 * G) iscr[32 + tid] = 0;
         const long long cap_cells = p.cap_cells;
         // chunk k*32 + lane of a 16-row sub-block: row k*RPI0 + lane/CPR, chunk lane%CPR; the
         // swizzled destination repeats with period P0 in k (precomputed per lane)
@@ -433,11 +439,11 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                             atomicAdd(p.totals + 1, (unsigned long long)__popc(m));
                         }
                     }
-                    if (p.counts) {
+                    if constexpr (CNT) {
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
                             const int v = lvk::warp_sum_int((gm >> g) & 1 ? scan : 0);
-                            if (lane == 0 && v) atomicAdd(p.counts + ((size_t)slot * G + g) * 4 + 2, v);
+                            if (lane == 0 && v) atomicAdd(iscr + 32 + g * 4 + 2, v);
                         }
                     }
                 }
@@ -754,7 +760,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         LV9_TRACE(5)
 
         // ---- statistics: lanes with the same g = lane % G hold that head's counts
-        if (p.counts) {
+        if constexpr (CNT) {
             int s0 = my_sel, s1 = my_att;
 #pragma unroll
             for (int of = 16; of >= G; of >>= 1) {
@@ -762,9 +768,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 s1 += __shfl_xor_sync(0xffffffffu, s1, of);
             }
             if (lane < G) {
-                int* c = p.counts + ((size_t)slot * G + lane) * 4;
-                if (s0) atomicAdd(c + 0, s0);
-                if (s1) atomicAdd(c + 1, s1);
+                if (s0) atomicAdd(iscr + 32 + lane * 4 + 0, s0);
+                if (s1) atomicAdd(iscr + 32 + lane * 4 + 1, s1);
             }
         }
         if (p.totals && lane == 0) {
@@ -776,6 +781,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 
         // ---- warp partials -> CTA partial [G][DP+2] (m, l, o)
         constexpr int Wd = G * (DP + 2);
+        constexpr int Wp = Wd + (CNT ? 4 * G : 0);  // the CTA's partial record: [G][DP+2] (then the counts [G][4])
         float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Wd] over the rings
         float* shw = red;                                           // [NW][G] weights
         __syncthreads();
@@ -795,7 +801,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
         }
         __syncthreads();
-        float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wd;
+        float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wp;
+        if (CNT && tid < 4 * G) reinterpret_cast<int*>(part + Wd)[tid] = iscr[32 + tid];
         for (int g = warp; g < G; g += NW) {  // warp g combines head g's NW warp headers, one warp per lane
             const float mw = lane < NW ? wred[lane * Wd + g * (DP + 2)] : -INFINITY;
             const float lw = lane < NW ? wred[lane * Wd + g * (DP + 2) + 1] : 0.0f;
@@ -830,26 +837,27 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         if (iscr[1]) {
             LV9_TRACE(8)
             // all nb partials travel in one round trip: headers and o rows staged together
-            const float* src = p.partial_ws + (size_t)slot * nb * Wd;
+            const float* src = p.partial_ws + (size_t)slot * nb * Wp;
             float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);  // scratch over the rings
             float* L = M + G;
             float* wgt = M + 2 * G;                        // [nb][G]
-            float* stg = wgt + ((nb * G + 3) / 4) * 4;     // [per_chunk][Wd]
+            float* stg = wgt + ((nb * G + 3) / 4) * 4;     // [per_chunk][Wp]
             constexpr int EPT = (G * DP + NTHR - 1) / NTHR;
-            const int per_chunk = (NW * Ge::PERW - (2 * G + nb * G + 4) * 4) / (Wd * 4);
+            const int per_chunk = (NW * Ge::PERW - (2 * G + nb * G + 4) * 4) / (Wp * 4);
+            int csum = 0;  // thread tid < 3 G: head tid / 3's count tid % 3 over the team
             float accr[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) accr[k] = 0.0f;
             for (int s0 = 0; s0 < nb; s0 += per_chunk) {
                 const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
-                const float2* cs = reinterpret_cast<const float2*>(src + (size_t)s0 * Wd);
-                for (int i = tid; i < cnt * Wd / 2; i += NTHR) reinterpret_cast<float2*>(stg)[i] = __ldcg(cs + i);
+                const float2* cs = reinterpret_cast<const float2*>(src + (size_t)s0 * Wp);
+                for (int i = tid; i < cnt * Wp / 2; i += NTHR) reinterpret_cast<float2*>(stg)[i] = __ldcg(cs + i);
                 __syncthreads();
                 if (s0 == 0) {
                     LV9_TRACE(11)
                     const bool one = cnt == nb;  // headers from the staged copy when it holds them all
                     auto hdr = [&](int s2, int g, int k) {
-                        return one ? stg[s2 * Wd + g * (DP + 2) + k] : __ldcg(src + (size_t)s2 * Wd + g * (DP + 2) + k);
+                        return one ? stg[s2 * Wp + g * (DP + 2) + k] : __ldcg(src + (size_t)s2 * Wp + g * (DP + 2) + k);
                     };
                     for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
                         float mm = -INFINITY;
@@ -872,6 +880,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     }
                     __syncthreads();
                 }
+                if (CNT && tid < 3 * G)
+                    for (int s2 = 0; s2 < cnt; ++s2) csum += reinterpret_cast<const int*>(stg + s2 * Wp + Wd)[(tid / 3) * 4 + tid % 3];
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int i = tid + k * NTHR;
@@ -879,7 +889,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         const int g = i / DP, c = i % DP;
                         float a = accr[k];
 #pragma unroll 6
-                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stg[s2 * Wd + g * (DP + 2) + 2 + c], a);
+                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stg[s2 * Wp + g * (DP + 2) + 2 + c], a);
                         accr[k] = a;
                     }
                 }
@@ -901,7 +911,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     p.partial_out[(size_t)slot * Wd + tid * (DP + 2)] = L[tid] > 0.0f ? M[tid] : -INFINITY;
                     p.partial_out[(size_t)slot * Wd + tid * (DP + 2) + 1] = L[tid];
                 }
-                if (p.counts) p.counts[((size_t)slot * G + tid) * 4 + 3] = L[tid] > 0.0f ? 1 : 0;
+                if (CNT) p.counts[((size_t)slot * G + tid) * 4 + 3] = L[tid] > 0.0f ? 1 : 0;
+            }
+            if (CNT && tid < 3 * G) {  // the team's selected / attended / scanned totals
+                p.counts[((size_t)slot * G + tid / 3) * 4 + tid % 3] = csum;
             }
             if (tid == 0) *ticket = 0;
             LV9_TRACE(7)

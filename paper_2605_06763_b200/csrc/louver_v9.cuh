@@ -758,6 +758,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
         }
         LV9_TRACE(5)
+        if (trace && lane == 0 && NW <= 16) trace[16 + warp] = gtimer();
 
         // ---- statistics: lanes with the same g = lane % G hold that head's counts
         if constexpr (CNT) {
@@ -836,40 +837,61 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         __syncthreads();
         if (iscr[1]) {
             LV9_TRACE(8)
-            // all nb partials travel in one round trip: headers and o rows staged together
+            // one round trip: every thread requests its o elements of CH partials into
+            // registers, the header warps request the (m, l) pairs alongside, and the
+            // weights are ready by the time the o values land
             const float* src = p.partial_ws + (size_t)slot * nb * Wp;
             float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);  // scratch over the rings
             float* L = M + G;
-            float* wgt = M + 2 * G;                        // [nb][G]
-            float* stg = wgt + ((nb * G + 3) / 4) * 4;     // [per_chunk][Wp]
+            float* wgt = M + 2 * G;  // [nb][G]
             constexpr int EPT = (G * DP + NTHR - 1) / NTHR;
-            const int per_chunk = (NW * Ge::PERW - (2 * G + nb * G + 4) * 4) / (Wp * 4);
+            constexpr int CH = EPT == 1 ? 24 : 12;  // partials per register chunk
             int csum = 0;  // thread tid < 3 G: head tid / 3's count tid % 3 over the team
+            if (CNT && tid < 3 * G) {
+                const int* cs = reinterpret_cast<const int*>(src + Wd) + (tid / 3) * 4 + tid % 3;
+#pragma unroll 8
+                for (int s2 = 0; s2 < nb; ++s2) csum += __ldcg(cs + (size_t)s2 * Wp);
+            }
             float accr[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) accr[k] = 0.0f;
-            for (int s0 = 0; s0 < nb; s0 += per_chunk) {
-                const int cnt = nb - s0 < per_chunk ? nb - s0 : per_chunk;
-                const float2* cs = reinterpret_cast<const float2*>(src + (size_t)s0 * Wp);
-                for (int i = tid; i < cnt * Wp / 2; i += NTHR) reinterpret_cast<float2*>(stg)[i] = __ldcg(cs + i);
-                __syncthreads();
+            for (int s0 = 0; s0 < nb; s0 += CH) {
+                const int cnt = nb - s0 < CH ? nb - s0 : CH;
+                float ov[EPT][CH];
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    const int i = tid + k * NTHR;
+                    const float* os = src + (size_t)s0 * Wp + (i / DP) * (DP + 2) + 2 + i % DP;
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) ov[k][j] = (i < G * DP && j < cnt) ? __ldcg(os + (size_t)j * Wp) : 0.0f;
+                }
                 if (s0 == 0) {
                     LV9_TRACE(11)
-                    const bool one = cnt == nb;  // headers from the staged copy when it holds them all
-                    auto hdr = [&](int s2, int g, int k) {
-                        return one ? stg[s2 * Wp + g * (DP + 2) + k] : __ldcg(src + (size_t)s2 * Wp + g * (DP + 2) + k);
-                    };
                     for (int g = warp; g < G; g += NW) {  // one warp per head: max, weights, l
-                        float mm = -INFINITY;
-                        for (int s2 = lane; s2 < nb; s2 += 32) mm = fmaxf(mm, hdr(s2, g, 0));
+                        float mh[2], lh[2];
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            const int s2 = lane + 32 * t;
+                            mh[t] = s2 < nb ? __ldcg(src + (size_t)s2 * Wp + g * (DP + 2)) : -INFINITY;
+                            lh[t] = s2 < nb ? __ldcg(src + (size_t)s2 * Wp + g * (DP + 2) + 1) : 0.0f;
+                        }
+                        float mm = fmaxf(mh[0], mh[1]);
+                        for (int s2 = lane + 64; s2 < nb; s2 += 32) mm = fmaxf(mm, __ldcg(src + (size_t)s2 * Wp + g * (DP + 2)));
 #pragma unroll
                         for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
                         float l = 0.0f;
-                        for (int s2 = lane; s2 < nb; s2 += 32) {
-                            const float ms = hdr(s2, g, 0);
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            const int s2 = lane + 32 * t;
+                            const float w = mh[t] == -INFINITY ? 0.0f : __expf(mh[t] - mm);
+                            if (s2 < nb) wgt[s2 * G + g] = w;
+                            l += w * lh[t];
+                        }
+                        for (int s2 = lane + 64; s2 < nb; s2 += 32) {
+                            const float ms = __ldcg(src + (size_t)s2 * Wp + g * (DP + 2));
                             const float w = ms == -INFINITY ? 0.0f : __expf(ms - mm);
                             wgt[s2 * G + g] = w;
-                            l += w * hdr(s2, g, 1);
+                            l += w * __ldcg(src + (size_t)s2 * Wp + g * (DP + 2) + 1);
                         }
 #pragma unroll
                         for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
@@ -880,20 +902,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                     }
                     __syncthreads();
                 }
-                if (CNT && tid < 3 * G)
-                    for (int s2 = 0; s2 < cnt; ++s2) csum += reinterpret_cast<const int*>(stg + s2 * Wp + Wd)[(tid / 3) * 4 + tid % 3];
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int i = tid + k * NTHR;
-                    if (i < G * DP) {
-                        const int g = i / DP, c = i % DP;
-                        float a = accr[k];
-#pragma unroll 6
-                        for (int s2 = 0; s2 < cnt; ++s2) a = fmaf(wgt[(s0 + s2) * G + g], stg[s2 * Wp + g * (DP + 2) + 2 + c], a);
-                        accr[k] = a;
-                    }
+                    const int g = (i / DP) < G ? i / DP : 0;
+                    float a = accr[k];
+#pragma unroll
+                    for (int j = 0; j < CH; ++j)
+                        if (j < cnt) a = fmaf(wgt[(s0 + j) * G + g], ov[k][j], a);
+                    accr[k] = a;
                 }
-                __syncthreads();
             }
             LV9_TRACE(14)
 #pragma unroll

@@ -69,12 +69,6 @@ def main():
             row.append(f"{(v.min() - t0) / 1e3:7.2f}/{(v.max() - t0) / 1e3:7.2f}" if v.size else " " * 15)
         print(f"{l:5d}  " + " ".join(f"{x:>16s}" for x in row))
     ends = [t[:, 7][t[:, 7] > 0].max() for t in trs]
-    for l, t in enumerate(trs):
-        w = t[t[:, 18] > 0]
-        if w.size:
-            d = lambda a, b: np.median(w[:, b] - w[:, a])
-            print(f"layer {l} merge body cycles: stage {d(18, 19):.0f}  heads {d(19, 20):.0f}  accumulate {d(20, 21):.0f}  "
-                  f"write {d(21, 22):.0f}")
     print(f"per-layer period (end to end): {np.diff(ends).mean() / 1e3:.2f} us")
     # merge body of the ticket winners: won -> partials staged (11) -> combined (14) -> end (7)
     seg = []
@@ -93,6 +87,17 @@ def main():
         par.extend(((w[:, 6] - w[:, 5]) / 1e3).tolist())
     if par:
         print(f"warp 0 tasks done -> CTA partial written: median {np.median(par):.2f} us")
+    # per CTA: first / last warp done with its tasks (16..31), last warp -> partial written
+    spread, red = [], []
+    for t in trs:
+        w = t[(t[:, 16] > 0) & (t[:, 6] > 0)]
+        wd = w[:, 16:32]
+        wd = np.where(wd > 0, wd, np.nan)
+        spread.extend(((np.nanmax(wd, 1) - np.nanmin(wd, 1)) / 1e3).tolist())
+        red.extend(((w[:, 6] - np.nanmax(wd, 1)) / 1e3).tolist())
+    if spread:
+        print(f"per CTA: warps' task-finish spread median {np.median(spread):.2f} us (max {np.max(spread):.2f}), "
+              f"last warp -> partial written median {np.median(red):.2f} us")
     # per slot (kv head): the team's survivor cells and when its last CTA finished its tasks
     nb = int(layers[0].geometry().get("team_ctas_per_slot", 18)) if hasattr(layers[0], "geometry") else 18
     for l in (1, 4):

@@ -172,7 +172,10 @@ size_t lv_query_workspace_bytes(const lv_ctx* ctx);
  * Each layer's query uses its context's internal workspace. With pinned buffers, the
  * internal staging and a non-default stream, the step runs as a CUDA graph captured on
  * the first call and replayed while the contexts, buffers and stream stay the same
- * (LV_LAYERS_GRAPH=0 disables it). */
+ * (LV_LAYERS_GRAPH=0 disables it). When the pinned buffers are mapped into the device
+ * address space (cudaHostAlloc memory on a UVA system) and d is a multiple of 64, the
+ * graph uses no copy engine: one kernel stages q and tau from host memory and each layer
+ * kernel writes its output rows straight into `out` (LV_LAYERS_MAPPED=0: copies). */
 int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau, float scale, int strict,
                     float* out, void* staging, void* stream);
 size_t lv_query_layers_staging_bytes(const lv_ctx* ctx, int L);

@@ -34,6 +34,7 @@ from .louver import (  # noqa: F401
     query_full_subspace,
     query_ta,
     query_layers_host,
+    LayersStep,
     sparse_attention,
     SubspaceIndex,
 )
@@ -41,7 +42,7 @@ from .louver import (  # noqa: F401
 __all__ = [
     "AttentionResult", "BuildConfig", "CacheQueryResult", "FilterAlgo", "LouverCache", "LouverLayer",
     "QueryRequest", "QueryStats", "CandidateSet", "SubspaceIndex", "query_ta", "query_full_subspace",
-    "derive_subspace_thresholds", "brute_force_range", "lse_merge", "query_layers_host", "sparse_attention", "LouverError",
+    "derive_subspace_thresholds", "brute_force_range", "lse_merge", "query_layers_host", "LayersStep", "sparse_attention", "LouverError",
     "ShardedLayer", "gather_partials", "insert_owner", "shard_range",
     "OracleConfig", "OracleVariant", "Reservoir", "estimate_tau", "estimate_tau_layer", "parse_oracle",
     "DecodeSimConfig", "MetricsReport", "ThresholdSource", "run_decode_sim", "GraphDecodeReport", "run_decode_graph",

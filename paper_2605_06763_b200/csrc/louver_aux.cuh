@@ -101,6 +101,22 @@ __global__ void __launch_bounds__(256) summarize_kernel(const T* __restrict__ K,
         atomicMax(reinterpret_cast<int*>(colmax + (size_t)slot * DP + c), __float_as_int(cmax[c]));
 }
 
+// Host-mapped (zero-copy) input staging for lv_query_layers: dst[i] = src[i] for the q
+// block and the tau block, read over the bus by many CTAs in one launch (a copy-engine
+// transfer costs ~10 us of fixed latency inside a graph; this costs one bus round trip).
+__global__ void stage_in_kernel(const float* __restrict__ q, float* __restrict__ qd, long long nq,
+                                const float* __restrict__ tau, float* __restrict__ td, long long nt) {
+    // the first layer kernel may launch now: it prefetches sealed summaries, then waits for this grid
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nq + nt;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (i < nq)
+            qd[i] = __ldcv(q + i);
+        else
+            td[i - nq] = __ldcv(tau + (i - nq));
+    }
+}
+
 // One decode step's insert for every slot (cache.cpp:7-10 on the device):
 // append k/v at row n, fold k into cell n/r's box (opening it when n % r == 0),
 // raise colmax; the last CTA advances n and applies the flush-at-B rule

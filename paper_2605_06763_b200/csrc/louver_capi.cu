@@ -887,6 +887,40 @@ int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau
         LV_CUDA(cudaMemcpyAsync(out, od, sizeof(float) * L * rows * d, cudaMemcpyDeviceToHost, st));
         return LV_OK;
     };
+    // Mapped (page-locked, UVA) host buffers: no copy-engine transfers at all. One launch
+    // stages every layer's q and tau from host memory, and each layer kernel writes its output
+    // rows straight into the host buffer (d == DP: the kernel's rows are the caller's rows).
+    const float *qm = nullptr, *tm = nullptr;
+    float* om = nullptr;
+    {
+        void* p = nullptr;
+        if (cudaHostGetDevicePointer(&p, const_cast<float*>(q), 0) == cudaSuccess) qm = static_cast<const float*>(p);
+        if (cudaHostGetDevicePointer(&p, const_cast<float*>(tau), 0) == cudaSuccess) tm = static_cast<const float*>(p);
+        if (cudaHostGetDevicePointer(&p, out, 0) == cudaSuccess) om = static_cast<float*>(p);
+        cudaGetLastError();
+        if (const char* e = std::getenv("LV_LAYERS_MAPPED"))  // 0: copy-engine transfers (A/B)
+            if (!std::atoi(e)) qm = nullptr;
+    }
+    const bool mapped = qm && tm && om && c0->DP == (int)d;
+    auto enqueue_mapped = [&]() -> int {
+        const long long nq = (long long)(L * rows * d), nt = (long long)(L * rows);
+        const unsigned blocks = (unsigned)std::min<long long>((nq + nt + 255) / 256, 4LL * c0->sms);
+        lvk::stage_in_kernel<<<blocks, 256, 0, st>>>(qm, qd, nq, tm, td, nt);
+        LV_CUDA(cudaGetLastError());
+        for (int l = 0; l < L; ++l) {
+            lv_query_args a{};
+            a.q = qd + (size_t)l * rows * d;
+            a.tau = td + (size_t)l * rows;
+            a.scale = scale;
+            a.algo = LV_ALGO_TA;
+            a.strict = strict;
+            a.where = LV_DEVICE;
+            a.out = om + (size_t)l * rows * d;
+            a.stream = stream;
+            if (int rc = lv_query(ctxs[l], &a)) return rc;
+        }
+        return LV_OK;
+    };
     // The step as a CUDA graph (one launch instead of 2 + L + 1, kernels scheduled back to back)
     // when it can be captured: a non-default stream that is not itself capturing, page-locked
     // host buffers, the context-internal staging (its lock serialises the calls).
@@ -902,7 +936,7 @@ int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau
         if (const char* e = std::getenv("LV_LAYERS_GRAPH")) graph = graph && std::atoi(e) != 0;
     }
     if (!graph) {
-        if (int rc = enqueue()) return rc;
+        if (int rc = mapped ? enqueue_mapped() : enqueue()) return rc;
         LV_CUDA(cudaStreamSynchronize(st));
         return LV_OK;
     }
@@ -914,7 +948,7 @@ int lv_query_layers(lv_ctx* const* ctxs, int L, const float* q, const float* tau
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g.exec = nullptr;
         LV_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        const int rc = enqueue();
+        const int rc = mapped ? enqueue_mapped() : enqueue();
         cudaGraph_t gr = nullptr;
         const cudaError_t e = cudaStreamEndCapture(st, &gr);
         if (rc) {

@@ -607,20 +607,43 @@ class LouverLayer:
         return out
 
 
-def query_layers_host(layers: Sequence["LouverLayer"], q: np.ndarray, tau: np.ndarray, out: np.ndarray, *,
-                      scale: float = 0.0, strict: bool = False, stream=None) -> np.ndarray:
-    """One decode step over L layers through the C ABI with HOST buffers (lv_query_layers):
-    q [L][batch][H_q][d], tau [L][batch][H_q], out [L][batch][H_q][d] float32, C-contiguous
-    (pinned for full speed). One copy in, L fused queries, one copy out, one sync."""
+def _layers_host_args(layers, q, tau, out, scale, strict, stream):
     L = len(layers)
     for a, shape in ((q, (L, layers[0].batch, layers[0].H_q, layers[0].d)), (tau, (L, layers[0].batch, layers[0].H_q)),
                      (out, (L, layers[0].batch, layers[0].H_q, layers[0].d))):
         if a.dtype != np.float32 or not a.flags.c_contiguous or a.shape != shape:
             raise ValueError(f"query_layers_host: expected C-contiguous float32 {shape}")
     hs = (C.c_void_p * L)(*[ly._ctx.h for ly in layers])
-    check(_capi.lib().lv_query_layers(hs, L, _ptr(q), _ptr(tau), float(scale), 1 if strict else 0, _ptr(out), None,
-                                      stream), "lv_query_layers")
+    return hs, (hs, L, _ptr(q), _ptr(tau), float(scale), 1 if strict else 0, _ptr(out), None, stream)
+
+
+def query_layers_host(layers: Sequence["LouverLayer"], q: np.ndarray, tau: np.ndarray, out: np.ndarray, *,
+                      scale: float = 0.0, strict: bool = False, stream=None) -> np.ndarray:
+    """One decode step over L layers through the C ABI with HOST buffers (lv_query_layers):
+    q [L][batch][H_q][d], tau [L][batch][H_q], out [L][batch][H_q][d] float32, C-contiguous
+    (pinned for full speed). Inputs go in per layer, L fused queries, outputs come back per
+    layer, one sync (see LayersStep for the repeated call)."""
+    _, args = _layers_host_args(layers, q, tau, out, scale, strict, stream)
+    check(_capi.lib().lv_query_layers(*args), "lv_query_layers")
     return out
+
+
+class LayersStep:
+    """query_layers_host prepared once for fixed buffers: the arguments are validated and
+    marshalled here, so each call is the one C call a C++ caller makes per decode step. The
+    caller rewrites q and tau in place between calls and reads out after each."""
+
+    def __init__(self, layers: Sequence["LouverLayer"], q: np.ndarray, tau: np.ndarray, out: np.ndarray, *,
+                 scale: float = 0.0, strict: bool = False, stream=None):
+        hs, self._args = _layers_host_args(layers, q, tau, out, scale, strict, stream)
+        self._keep = (list(layers), q, tau, out, hs)
+        self._fn = _capi.lib().lv_query_layers
+
+    def __call__(self) -> np.ndarray:
+        rc = self._fn(*self._args)
+        if rc:
+            check(rc, "lv_query_layers")
+        return self._keep[3]
 
 
 def lse_merge(partials, out, stream=None) -> None:

@@ -135,11 +135,16 @@ def test_query_layers_host_equals_device_queries(torch):
         query_layers_host(layers, q[:, :, :4], t, out)
 
 
-def test_query_layers_graph_follows_inputs_inserts_and_growth(torch):
+@pytest.mark.parametrize("mapped", [1, 0])
+def test_query_layers_graph_follows_inputs_inserts_and_growth(torch, monkeypatch, mapped):
     """lv_query_layers replays a cached CUDA graph when its buffers are pinned and the stream
     is not the default one: new q contents, keys pushed between steps and an arena that grew
-    (lv_reserve) must all be reflected, exactly as per-layer device queries see them."""
+    (lv_reserve) must all be reflected, exactly as per-layer device queries see them. Both
+    graph forms: mapped host buffers (a staging kernel in, outputs written by the layer
+    kernels) and copy-engine transfers (LV_LAYERS_MAPPED=0)."""
     from paper_2605_06763_b200 import query_layers_host
+
+    monkeypatch.setenv("LV_LAYERS_MAPPED", str(mapped))
 
     L, H, G, d, n = 2, 2, 4, 128, 2000
     layers = []

@@ -181,6 +181,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     }
     float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
+    // C tile element (r, c) at r CT + c with its 16-byte chunk XORed by (r >> 1) mod CS: the
+    // accumulator stores (8 rows x 4 lanes) and the per-row reads then hit distinct banks
+    constexpr int CS = (CT / 4) % 4 == 0 ? 4 : 2;
+    auto cto = [](int r, int c) { return r * CT + ((((c >> 2) ^ ((r >> 1) & (CS - 1))) << 2) | (c & 3)); };
     const int q4 = lane & 3;
     // per-lane ldmatrix offsets: A (rows = keys / cells) and V^T (trans)
     const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
@@ -405,8 +409,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int nt = 0; nt < NTP; ++nt) {
                         const int rw = lane >> 2, col = nt * 8 + 2 * q4;
-                        *reinterpret_cast<float2*>(ct + rw * CT + col) = make_float2(acc[nt][0], acc[nt][1]);
-                        *reinterpret_cast<float2*>(ct + (rw + 8) * CT + col) = make_float2(acc[nt][2], acc[nt][3]);
+                        *reinterpret_cast<float2*>(ct + cto(rw, col)) = make_float2(acc[nt][0], acc[nt][1]);
+                        *reinterpret_cast<float2*>(ct + cto(rw + 8, col)) = make_float2(acc[nt][2], acc[nt][3]);
                     }
                     __syncwarp();
                     unsigned gm = 0;
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         } else {
 #pragma unroll
                             for (int g = 0; g < G; ++g)
-                                if (ct[lane * CT + g] + ct[lane * CT + G + g] >= taup[g]) gm |= 1u << g;
+                                if (ct[cto(lane, g)] + ct[cto(lane, G + g)] >= taup[g]) gm |= 1u << g;
                         }
                         scan = (int)((ce < n ? ce : n) - cs);
                     }
@@ -573,8 +577,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
                         const int rw = lane >> 2, col = nt * 8 + 2 * q4;
-                        *reinterpret_cast<float2*>(ct + rw * CT + col) = make_float2(acc[nt][0], acc[nt][1]);
-                        *reinterpret_cast<float2*>(ct + (rw + 8) * CT + col) = make_float2(acc[nt][2], acc[nt][3]);
+                        *reinterpret_cast<float2*>(ct + cto(rw, col)) = make_float2(acc[nt][0], acc[nt][1]);
+                        *reinterpret_cast<float2*>(ct + cto(rw + 8, col)) = make_float2(acc[nt][2], acc[nt][3]);
                     }
                 }
                 __syncwarp();
@@ -584,8 +588,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) {
                     const int pi = lane + 32 * j, rw = pi / G;
-                    const float* c = ct + (rw < 16 ? rw : 15) * CT;
-                    const float sc = (c[g_me] + c[G + g_me]) + c[2 * G + g_me];
+                    const int rc = rw < 16 ? rw : 15;
+                    const float sc = (ct[cto(rc, g_me)] + ct[cto(rc, G + g_me)]) + ct[cto(rc, 2 * G + g_me)];
                     const bool valid = (G > 1 || lane < 16) && k0 + rw < n32;
                     const bool sel = valid && (DENSE || sc >= tau_me + marg_me);
                     const bool u = !DENSE && valid && !sel && sc >= tau_me - marg_me;

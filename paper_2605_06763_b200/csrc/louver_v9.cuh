@@ -787,21 +787,24 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         // ---- warp partials -> CTA partial [G][DP+2] (m, l, o)
         constexpr int Wd = G * (DP + 2);
         constexpr int Wp = Wd + (CNT ? 4 * G : 0);  // the CTA's partial record: [G][DP+2] (then the counts [G][4])
-        float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Wd] over the rings
+        // in shared memory a head's row is DP + 4 floats (== 4 mod 32 banks): the o stores of
+        // the lanes' (head, column) pairs below then hit distinct banks
+        constexpr int WP = DP + 4, Ws = G * WP;
+        float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Ws] over the rings
         float* shw = red;                                           // [NW][G] weights
         __syncthreads();
         {
-            float* w = wred + warp * Wd;
+            float* w = wred + warp * Ws;
             if (lane < G) {
-                w[lane * (DP + 2)] = mrun * 0.6931471805599453f;  // back to nats
-                w[lane * (DP + 2) + 1] = lpart;
+                w[lane * WP] = mrun * 0.6931471805599453f;  // back to nats
+                w[lane * WP + 1] = lpart;
             }
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int h = 2 * q4 + (e & 1), c = 16 * mt + (lane >> 2) + 8 * (e >> 1);
-                    if (h < G) w[h * (DP + 2) + 2 + c] = o[mt][e];
+                    if (h < G) w[h * WP + 2 + c] = o[mt][e];
                 }
             }
         }
@@ -809,8 +812,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wp;
         if (CNT && tid < 4 * G) reinterpret_cast<int*>(part + Wd)[tid] = iscr[32 + tid];
         for (int g = warp; g < G; g += NW) {  // warp g combines head g's NW warp headers, one warp per lane
-            const float mw = lane < NW ? wred[lane * Wd + g * (DP + 2)] : -INFINITY;
-            const float lw = lane < NW ? wred[lane * Wd + g * (DP + 2) + 1] : 0.0f;
+            const float mw = lane < NW ? wred[lane * Ws + g * WP] : -INFINITY;
+            const float lw = lane < NW ? wred[lane * Ws + g * WP + 1] : 0.0f;
             float mm = mw;
 #pragma unroll
             for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
@@ -829,7 +832,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             const int g = i / DP, c = i % DP;
             float s = 0.0f;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * Wd + g * (DP + 2) + 2 + c], s);
+            for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * Ws + g * WP + 2 + c], s);
             part[g * (DP + 2) + 2 + c] = s;
         }
         LV9_TRACE(6)

@@ -181,10 +181,16 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     }
     float* ct = reinterpret_cast<float*>(wbase + 3 * Ge::STAGE);
     float* pbuf = ct + 16 * CT;
-    // C tile element (r, c) at r CT + c with its 16-byte chunk XORed by (r >> 1) mod CS: the
-    // accumulator stores (8 rows x 4 lanes) and the per-row reads then hit distinct banks
-    constexpr int CS = (CT / 4) % 4 == 0 ? 4 : 2;
-    auto cto = [](int r, int c) { return r * CT + ((((c >> 2) ^ ((r >> 1) & (CS - 1))) << 2) | (c & 3)); };
+    // C tile element (r, c) at r CT + c, its 16-byte chunk XORed with the bit-reversed
+    // (r >> 1) & 3 when rows are 16 floats (mod 32 banks): the accumulator stores (rows r,
+    // r + 2 of a half-warp get disjoint chunk pairs) and the per-row reads (rows of equal
+    // parity get distinct chunks) are then bank-conflict free. Other pitches need no swizzle.
+    constexpr bool CSW = CT % 32 == 16;
+    auto cto = [](int r, int c) {
+        if constexpr (!CSW) return r * CT + c;
+        const int x = (r >> 1) & 3, f = ((x & 1) << 1) | (x >> 1);
+        return r * CT + ((((c >> 2) ^ f) << 2) | (c & 3));
+    };
     const int q4 = lane & 3;
     // per-lane ldmatrix offsets: A (rows = keys / cells) and V^T (trans)
     const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;

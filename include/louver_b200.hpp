@@ -659,6 +659,18 @@ class LouverLayer {
     std::unique_ptr<lv_ctx, detail::CtxDeleter> ctx_;
 };
 
+// One decode step over L layers with HOST buffers (lv_query_layers): q [L][rows][d],
+// tau [L][rows], out [L][rows][d] fp32. With cudaHostAlloc'd buffers and a non-default
+// stream the step is a cached CUDA graph with no copy-engine transfers.
+inline void query_layers_host(const std::vector<const LouverLayer*>& layers, const float* q, const float* tau,
+                              float* out, cudaStream_t st, float scale = 0.0f, bool strict = false) {
+    std::vector<lv_ctx*> hs;
+    hs.reserve(layers.size());
+    for (const LouverLayer* l : layers) hs.push_back(l->handle());
+    detail::check(lv_query_layers(hs.data(), static_cast<int>(hs.size()), q, tau, scale, strict ? 1 : 0, out, nullptr, st),
+                  "lv_query_layers");
+}
+
 // Log-sum-exp merge of P sequence-shard partials [P][rows][d+2] -> out [rows][d].
 inline void lse_merge(const float* partials, int P, std::int64_t rows, int d, float* out, cudaStream_t st) {
     detail::check(lv_lse_merge(partials, P, rows, d, out, st), "lv_lse_merge");

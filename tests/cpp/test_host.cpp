@@ -274,6 +274,30 @@ static void test_layer_bf16() {
         EXPECT(rel_err(out.data() + hq * d, o.data(), d) <= 1e-4, "head %d attention rel err %g", hq,
                rel_err(out.data() + hq * d, o.data(), d));
     }
+    // the host-buffer decode step (lv_query_layers) with mapped pinned buffers on a
+    // non-default stream: the cached graph, called twice (capture, replay)
+    float *hq, *ht, *ho;
+    cudaHostAlloc(reinterpret_cast<void**>(&hq), Q.size() * 4, cudaHostAllocDefault);
+    cudaHostAlloc(reinterpret_cast<void**>(&ht), tau.size() * 4, cudaHostAllocDefault);
+    cudaHostAlloc(reinterpret_cast<void**>(&ho), Q.size() * 4, cudaHostAllocDefault);
+    std::copy(Q.begin(), Q.end(), hq);
+    std::copy(tau.begin(), tau.end(), ht);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    for (int rep = 0; rep < 2; ++rep) {
+        std::fill(ho, ho + Q.size(), 0.0f);
+        query_layers_host({&layer}, hq, ht, ho, st);
+        double worst = 0.0, scale = 0.0;
+        for (size_t i = 0; i < out.size(); ++i) {
+            worst = std::max(worst, (double)std::fabs(ho[i] - out[i]));
+            scale = std::max(scale, (double)std::fabs(out[i]));
+        }
+        EXPECT(worst <= 1e-5 * scale, "query_layers_host (call %d) vs query_device: max diff %g", rep, worst);
+    }
+    cudaStreamDestroy(st);
+    cudaFreeHost(hq);
+    cudaFreeHost(ht);
+    cudaFreeHost(ho);
     cudaFree(dq);
     cudaFree(dt);
     cudaFree(dout);

@@ -58,7 +58,17 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE, CNT>, vp);
+    cudaError_t e;
+    if constexpr (!CNT) {
+        if (nb == 1) {  // teams of one: the instantiation without the team merge
+            const void* fn1 = reinterpret_cast<const void*>(louver_layer_v9<DP, G, DENSE, false, true>);
+            if ((e = lvl::func_smem(fn1, smem)) != cudaSuccess) return e;
+            e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE, false, true>, vp);
+            if (e != cudaSuccess) return e;
+            return cudaGetLastError();
+        }
+    }
+    e = cudaLaunchKernelEx(&cfg, louver_layer_v9<DP, G, DENSE, CNT>, vp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

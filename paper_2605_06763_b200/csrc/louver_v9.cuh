@@ -139,8 +139,11 @@ struct C9 {
 };
 
 // CNT: the launch writes p.counts (an instantiation of its own, so that the launches
-// without statistics — the bench, the production decode step — keep their code)
-template <int DP, int G, bool DENSE, bool CNT>
+// without statistics — the bench, the production decode step — keep their code).
+// SOLO: the launch has teams of one CTA (many slots, e.g. C3): the CTA's partial is the
+// slot's result and is written out directly, with no ticket (also its own instantiation,
+// so that the team path keeps its code).
+template <int DP, int G, bool DENSE, bool CNT, bool SOLO = false>
 __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer_v9(const __grid_constant__ LayerParams vp) {
     using Ge = C9<DP, G>;
     constexpr bool PACK = G <= 4;  // P.V: hi and lo parts of P share one n-tile
@@ -846,6 +849,26 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         // ---- phase C: the last CTA of the team merges the nb partials
         int* ticket = vp.stickets + slot;
         __syncthreads();
+        if constexpr (SOLO) {  // a team of one (nb == 1): its partial is the result, no ticket
+            for (int i = tid; i < G * DP; i += NTHR) {
+                const int g = i / DP, c = i % DP;
+                const float l = __ldcg(part + g * (DP + 2) + 1), o = __ldcg(part + g * (DP + 2) + 2 + c);
+                if (p.out) p.out[((size_t)slot * G + g) * DP + c] = l > 0.0f ? o / l : 0.0f;
+                if (p.partial_out) p.partial_out[(size_t)slot * Wd + g * (DP + 2) + 2 + c] = o;
+            }
+            if (tid < G) {
+                const float m = __ldcg(part + tid * (DP + 2)), l = __ldcg(part + tid * (DP + 2) + 1);
+                if (p.partial_out) {
+                    p.partial_out[(size_t)slot * Wd + tid * (DP + 2)] = m;
+                    p.partial_out[(size_t)slot * Wd + tid * (DP + 2) + 1] = l;
+                }
+                if (CNT) p.counts[((size_t)slot * G + tid) * 4 + 3] = l > 0.0f ? 1 : 0;
+            }
+            if (CNT && tid < 3 * G) p.counts[((size_t)slot * G + tid / 3) * 4 + tid % 3] = iscr[32 + (tid / 3) * 4 + tid % 3];
+            __syncthreads();
+            __syncthreads();  // (as at the end of the merge: the rings are reused by the next slot)
+            continue;
+        }
         if (tid == 0) iscr[1] = atom_add_acq_rel(ticket, 1) == nb - 1;
         __syncthreads();
         if (iscr[1]) {

@@ -190,8 +190,8 @@ int lv_geometry(const lv_ctx* ctx, int64_t* out);
  * by the last query launch; zeros before the first bf16 query. */
 int lv_layer_geometry(const lv_ctx* ctx, int64_t* out);
 
-/* Debug: while dev_buf != NULL, bf16 queries write 16 globaltimer stamps per
- * CTA (order [slot][team CTA]) into dev_buf [slots*team][16]. */
+/* Debug: while dev_buf != NULL, bf16 queries write up to 64 globaltimer stamps per
+ * CTA (order [slot][team CTA]) into dev_buf [slots*team][64]. */
 int lv_debug_trace(lv_ctx* ctx, int64_t* dev_buf);
 int64_t lv_bitmap_words(const lv_ctx* ctx);
 

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     // with rows past n zero-filled, so rows that are not attended hold finite values)
 
     for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
-        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 32 : nullptr;
+        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 64 : nullptr;
         LV9_TRACE(0)
         const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
         const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (c0 >= ncells) break;
                 cpa_wait<2>();  // sub-block u landed (u + 1, u + 2 may pend)
                 __syncwarp();
+                if (trace && lane == 0 && NW <= 16 && u == 0) trace[48 + warp] = gtimer();
                 const int half = u & 1;
                 if (half == 0) {
 #pragma unroll
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
             cpa_wait<0>();
             __syncwarp();
+            if (trace && lane == 0 && NW <= 16) trace[32 + warp] = gtimer();
         }
         LV9_TRACE(2)
 

@@ -31,7 +31,7 @@ def main():
         taus.append(torch.from_numpy(bench.taus_device(torch, K, Q, G, bench.SELECTIVITY)).cuda())
         outs.append(torch.zeros((cfg["batch"], cfg["H_kv"] * G, cfg["d"]), device="cuda"))
         slots = cfg["batch"] * cfg["H_kv"]
-        buf = torch.zeros((slots * 148, 32), dtype=torch.int64, device="cuda")
+        buf = torch.zeros((slots * 148, 64), dtype=torch.int64, device="cuda")
         layer._ctx.lib.lv_debug_trace(layer._ctx.h, buf.data_ptr())
         bufs.append(buf)
 
@@ -95,6 +95,17 @@ def main():
         wd = np.where(wd > 0, wd, np.nan)
         spread.extend(((np.nanmax(wd, 1) - np.nanmin(wd, 1)) / 1e3).tolist())
         red.extend(((w[:, 6] - np.nanmax(wd, 1)) / 1e3).tolist())
+    # probe: setup done (1) -> first sub-block available (48..63) / warp's probe done (32..47)
+    a0, pe = [], []
+    for t in trs:
+        w = t[(t[:, 1] > 0) & (t[:, 48] > 0)]
+        f0 = np.where(w[:, 48:64] > 0, w[:, 48:64], np.nan)
+        pd = np.where(w[:, 32:48] > 0, w[:, 32:48], np.nan)
+        a0.extend((np.nanmax(f0, 1) - w[:, 1]).tolist())
+        pe.extend(((np.nanmax(pd, 1) - w[:, 1]) / 1e3).tolist())
+    if a0:
+        print(f"probe: setup done -> slowest warp's first sub-block available: median {np.median(a0) / 1e3:.2f} us; "
+              f"-> last warp's probe done: median {np.median(pe):.2f} us (max {np.max(pe):.2f})")
     if spread:
         print(f"per CTA: warps' task-finish spread median {np.median(spread):.2f} us (max {np.max(spread):.2f}), "
               f"last warp -> partial written median {np.median(red):.2f} us")

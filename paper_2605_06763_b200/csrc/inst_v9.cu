@@ -36,6 +36,15 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
     const int cap = occ * sms;
     int gy = cap / nb;
     if (gy > slots) gy = slots;
+    // Every slot resident and SMs left over (148 over 8 slots: 4 idle with teams of 18):
+    // the first cap - nb slots get one CTA more (lists sized for the smaller team, partial
+    // records for vp.nb per slot; vp.nfull != 0 on entry allows it)
+    int nfull = slots;
+    if (vp.nfull && !glist && gy == slots && nb >= 2 && nb + 1 <= vp.nb && cap > nb * slots) {
+        nfull = cap - nb * slots < slots ? cap - nb * slots : slots;
+        ++nb;
+    }
+    vp.nfull = nfull;
     vp.nb = nb;
     vp.slots = slots;
     if (geo) {  // team CTAs per slot, threads per CTA, dynamic smem, resident CTAs per SM

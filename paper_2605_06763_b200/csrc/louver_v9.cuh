@@ -47,13 +47,15 @@ struct LayerParams {
     QueryParams p;
     const __nv_bfloat16* sum;  // [slot][cap_cells][2*DP] cell rows [hi | lo]
     int* stickets;             // [slots] merge tickets (self-resetting)
-    int nb;                    // team CTAs per slot
+    int nb;                    // team CTAs per slot (slots >= nfull: nb - 1)
+    int nfull;                 // slots with teams of nb CTAs (148 SMs over 8 slots: 4 of 19, 4 of 18)
     int slots;                 // slots of the layer (the grid may loop over them)
     unsigned short* glist;     // survivor lists in global scratch when they outgrow smem (else null)
     int list_cap;              // entries per CTA list
     long long sealed;          // cells complete when the query was enqueued (immutable summaries)
     int npre;                  // summary sub-blocks requested before griddepcontrol.wait (0..3)
     int ktma;                  // key blocks by TMA (kmap) instead of cp.async
+    int kpf;                   // the CTA's first kpf listed cells: key blocks L2-prefetched by the probe
     alignas(64) CUtensorMap kmap;  // K arena as [slots * cap][DP] bf16, box 64 x 16, 128-byte swizzle
 };
 
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     // global scratch when the list outgrows shared memory
     unsigned short* slist_s = reinterpret_cast<unsigned short*>(smem + Ge::DYN);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int blk = blockIdx.x, nb = vp.nb;
+    const int blk = blockIdx.x, nbs = vp.nb;  // partial records / lists / traces: nbs per slot
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
     const unsigned ring = smem_u32(wbase);
     const int b7 = (int)((ring >> 7) & 7u);  // the same for every stage of the warp (4 KiB apart)
@@ -216,7 +218,9 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     // with rows past n zero-filled, so rows that are not attended hold finite values)
 
     for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
-        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nb + blk) * 64 : nullptr;
+        const int nb = slot < vp.nfull ? nbs : nbs - 1;  // this slot's team
+        if (blk >= nb) continue;                         // (uniform per CTA)
+        trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nbs + blk) * 64 : nullptr;
         LV9_TRACE(0)
         const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(p.K) + (size_t)slot * p.cap * DP;
         const __nv_bfloat16* Vs = reinterpret_cast<const __nv_bfloat16*>(p.V) + (size_t)slot * p.cap * DP;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         // split evenly with no team-wide exchange). CTA-local tile j = cells
         // blk + (16 j + i) nb, i < 16; warp w takes tiles w, w + NW, ...
         // Sub-task u of a warp: tile warp + (u >> 1) NW, half u & 1 ([hi] or [lo] rows).
-        unsigned short* slist = vp.glist ? vp.glist + ((size_t)slot * nb + blk) * vp.list_cap : slist_s;
+        unsigned short* slist = vp.glist ? vp.glist + ((size_t)slot * nbs + blk) * vp.list_cap : slist_s;
         if (tid == 0) {
             iscr[2] = 0;  // survivors listed
             iscr[3] = 0;  // tasks claimed
@@ -442,9 +446,14 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                         int base = 0;
                         if (lane == 0) base = atomicAdd(iscr + 2, __popc(m));
                         base = __shfl_sync(0xffffffffu, base, 0);
-                        if (gm)
-                            slist[base + __popc(m & ((1u << lane) - 1u))] =
-                                (unsigned short)(16 * (warp + (u >> 1) * NW) + lane);
+                        if (gm) {
+                            const int at = base + __popc(m & ((1u << lane) - 1u));
+                            slist[at] = (unsigned short)(16 * (warp + (u >> 1) * NW) + lane);
+                            // the survivor's key blocks are requested into L2 now: the HBM is
+                            // mostly idle while the probe finishes, and the exact phase that
+                            // follows is HBM-bound (its first tasks then hit in L2)
+                            if (at < vp.kpf) bulk_prefetch_l2(Ks + ((size_t)cell << rl) * DP, (unsigned)(RB << rl));
+                        }
                     }
                     if (p.totals) {
                         const int tested = __popc(__ballot_sync(0xffffffffu, lane < 16 && cell < ncells));
@@ -820,7 +829,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             }
         }
         __syncthreads();
-        float* part = p.partial_ws + ((size_t)slot * nb + blk) * Wp;
+        float* part = p.partial_ws + ((size_t)slot * nbs + blk) * Wp;
         if (CNT && tid < 4 * G) reinterpret_cast<int*>(part + Wd)[tid] = iscr[32 + tid];
         for (int g = warp; g < G; g += NW) {  // warp g combines head g's NW warp headers, one warp per lane
             const float mw = lane < NW ? wred[lane * Ws + g * WP] : -INFINITY;
@@ -878,7 +887,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             // one round trip: every thread requests its o elements of CH partials into
             // registers, the header warps request the (m, l) pairs alongside, and the
             // weights are ready by the time the o values land
-            const float* src = p.partial_ws + (size_t)slot * nb * Wp;
+            const float* src = p.partial_ws + (size_t)slot * nbs * Wp;
             float* M = reinterpret_cast<float*>(smem + Ge::OFF_W);  // scratch over the rings
             float* L = M + G;
             float* wgt = M + 2 * G;  // [nb][G]

@@ -54,7 +54,8 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
         geo[3] = occ;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)nb, (unsigned)gy);
+    if (gy != slots) vp.spread = 0;
+    cfg.gridDim = vp.spread ? dim3((unsigned)gy, (unsigned)nb) : dim3((unsigned)nb, (unsigned)gy);
     cfg.blockDim = dim3(Ge::NTHR);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;

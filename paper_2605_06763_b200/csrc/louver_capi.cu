@@ -105,6 +105,8 @@ struct lv_ctx {
     long long* trace = nullptr;  // debug: per-CTA phase timestamps of the bf16 query kernel
     lvg::GroupIndex* gi = nullptr;  // the reference's grouped index (cfg.group_index)
     int kpf = 8;                    // listed cells whose key blocks the probe L2-prefetches (LV_KPF)
+    int vtail = 16;                 // last tasks whose value blocks are L2-prefetched (LV_VTAIL)
+    int spread = 1;                 // late-dispatched CTAs spread over the slots (LV_SPREAD)
     int uneven = 1;                 // teams of nb and nb - 1 CTAs to fill every SM (LV_UNEVEN)
     int ktma = 0;                   // key blocks by TMA in the bf16 layer kernel (LV_KTMA=1; A/B: slower)
     int f32_layer = 1;               // fp32 queries on the fused fp32 layer kernel (LV_F32_LAYER=0: round-1 kernel)
@@ -190,6 +192,8 @@ void choose_splits(lv_ctx* c) {
         if (const char* e = std::getenv("LV_KTMA")) c->ktma = std::atoi(e);
         if (const char* e = std::getenv("LV_KPF")) c->kpf = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("LV_UNEVEN")) c->uneven = std::atoi(e);
+        if (const char* e = std::getenv("LV_VTAIL")) c->vtail = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("LV_SPREAD")) c->spread = std::atoi(e);
         if (const char* e = std::getenv("LV_F32_LAYER")) c->f32_layer = std::atoi(e);
         c->nb = (int)std::min<long long>(nb, 4096);
     }
@@ -367,6 +371,8 @@ int run_query_kernel(lv_ctx* c, int mode, const float* qdev, const float* taudev
         lp.npre = c->npre;
         lp.kpf = c->kpf;
         lp.nfull = c->uneven;
+        lp.vtail = c->vtail;
+        lp.spread = c->spread;
         lp.ktma = c->ktma && c->kmap_K == c->K;  // the map is encoded by lv_create / lv_reserve
         if (lp.ktma) lp.kmap = c->kmap;
         // cells complete before the last insert enqueued ahead of this query: the insert kernel

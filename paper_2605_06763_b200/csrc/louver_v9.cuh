@@ -56,6 +56,8 @@ struct LayerParams {
     int npre;                  // summary sub-blocks requested before griddepcontrol.wait (0..3)
     int ktma;                  // key blocks by TMA (kmap) instead of cp.async
     int kpf;                   // the CTA's first kpf listed cells: key blocks L2-prefetched by the probe
+    int vtail;                 // the CTA's last vtail tasks: value blocks L2-prefetched when claimed
+    int spread;                // grid (slots, team): the CTAs dispatched last are one member of each slot
     alignas(64) CUtensorMap kmap;  // K arena as [slots * cap][DP] bf16, box 64 x 16, 128-byte swizzle
 };
 
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     // global scratch when the list outgrows shared memory
     unsigned short* slist_s = reinterpret_cast<unsigned short*>(smem + Ge::DYN);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int blk = blockIdx.x, nbs = vp.nb;  // partial records / lists / traces: nbs per slot
+    const int blk = vp.spread ? blockIdx.y : blockIdx.x, nbs = vp.nb;  // records / lists / traces: nbs per slot
     unsigned char* wbase = smem + Ge::OFF_W + warp * Ge::PERW;
     const unsigned ring = smem_u32(wbase);
     const int b7 = (int)((ring >> 7) & 7u);  // the same for every stage of the warp (4 KiB apart)
@@ -217,7 +219,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
     // (no ring zeroing: a V stage is always the stage of its task's K block, loaded whole,
     // with rows past n zero-filled, so rows that are not attended hold finite values)
 
-    for (int slot = blockIdx.y; slot < vp.slots; slot += gridDim.y) {
+    const int slot0 = vp.spread ? blockIdx.x : blockIdx.y, sstep = vp.spread ? gridDim.x : gridDim.y;
+    for (int slot = slot0; slot < vp.slots; slot += sstep) {
         const int nb = slot < vp.nfull ? nbs : nbs - 1;  // this slot's team
         if (blk >= nb) continue;                         // (uniform per CTA)
         trace = p.tot_trace ? p.tot_trace + ((size_t)slot * nbs + blk) * 64 : nullptr;
@@ -568,6 +571,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
                 if (lane == 0 && tn < ntask) cb = atomicAdd(iscr + 3, 1);
                 const int kn = tn < ntask ? key0(tn) : 0;
                 k_issue(tn, kn, s1);
+                // the CTA's last tasks end on the chain K round trip -> scores -> V round trip:
+                // their value blocks are requested into L2 with the keys
+                if (lane == 0 && tn < ntask && tn >= ntask - vp.vtail)
+                    bulk_prefetch_l2(Vs + (size_t)kn * DP, 16 * RB);
                 if (ktma) {  // K(t) landed
                     mbar_wait(kbar + 8 * st, (kph >> st) & 1u);
                     kph ^= 1u << st;

@@ -407,7 +407,11 @@ def main():
     b_qo = rows * (d * 4 * 2 + 4)
     geo = layers[0].geometry()
     team = geo.get("team_ctas_per_slot") or geo["splits"]  # bf16: fused kernel team; fp32: splits
-    b_part = slots * team * G * (d + 2) * 4 * 2
+    ctas = slots * team
+    if geo.get("ctas_per_sm"):  # bf16 teams of nb and nb - 1 CTAs fill the resident wave exactly
+        ctas = min(ctas, geo["ctas_per_sm"] * torch.cuda.get_device_properties(0).multi_processor_count)
+    geo["layer_ctas"] = int(ctas)
+    b_part = ctas * G * (d + 2) * 4 * 2
     alg_bytes = float(np.mean(b_sum + b_key + b_val)) + b_qo + b_part
     dense_bytes = float(slots * n * d * e * 2 + b_qo)
     keys_scanned = float(np.mean(cnt[..., 2]))

@@ -403,6 +403,21 @@ def test_layer_query_many_cells_per_cta(torch, oracle):
     check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
 
 
+@pytest.mark.parametrize("H_kv,batch,n", [(3, 2, 26000), (5, 1, 31000)])
+@pytest.mark.parametrize("spread", ["0", "1"])
+def test_layer_query_uneven_teams(torch, oracle, monkeypatch, H_kv, batch, n, spread):
+    """148 SMs over 6 (5) slots: teams of 25 and 24 (30 and 29) CTAs, so every SM works; the
+    slots past the first cap - nb*slots hold one CTA less (partial records and survivor lists
+    strided by the larger team), with either grid order (LV_SPREAD)."""
+    monkeypatch.setenv("LV_SPREAD", spread)
+    layer, K, V, Q = make_layer(torch, oracle, H_kv=H_kv, G=4, batch=batch, n=n, r=16, seed=61 + H_kv)
+    tau = taus_at(oracle, K, Q, 4, 0.05)
+    check_layer(torch, oracle, layer, K, V, Q, tau, anchored=True)
+    if torch.cuda.get_device_properties(0).multi_processor_count == 148:
+        slots = H_kv * batch
+        assert layer.geometry()["team_ctas_per_slot"] == -(-148 // slots)
+
+
 def test_layer_iid_queries_and_extreme_taus(torch, oracle):
     layer, K, V, Q = make_layer(torch, oracle, H_kv=1, G=4, batch=1, n=2048, r=16)
     Qi = synth.iid_normal(4, 128, 5).reshape(1, 4, 128)

@@ -816,12 +816,15 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         constexpr int Wp = Wd + (CNT ? 4 * G : 0);  // the CTA's partial record: [G][DP+2] (then the counts [G][4])
         // in shared memory a head's row is DP + 4 floats (== 4 mod 32 banks): the o stores of
         // the lanes' (head, column) pairs below then hit distinct banks
-        constexpr int WP = DP + 4, Ws = G * WP;
-        float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][Ws] over the rings
+        constexpr int WP = DP + 4;
+        static_assert(G * (DP + 4) * 4 <= Ge::PERW, "a warp partial fits its ring area");
+        // warp w's partial sits at the start of its own ring area (free once its tasks are
+        // done), so a warp writes it as soon as it finishes, with no CTA barrier in front
+        constexpr int WS = Ge::PERW / 4;                            // warp stride in floats
+        float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][WS]
         float* shw = red;                                           // [NW][G] weights
-        __syncthreads();
         {
-            float* w = wred + warp * Ws;
+            float* w = wred + warp * WS;
             if (lane < G) {
                 w[lane * WP] = mrun * 0.6931471805599453f;  // back to nats
                 w[lane * WP + 1] = lpart;
@@ -839,8 +842,8 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         float* part = p.partial_ws + ((size_t)slot * nbs + blk) * Wp;
         if (CNT && tid < 4 * G) reinterpret_cast<int*>(part + Wd)[tid] = iscr[32 + tid];
         for (int g = warp; g < G; g += NW) {  // warp g combines head g's NW warp headers, one warp per lane
-            const float mw = lane < NW ? wred[lane * Ws + g * WP] : -INFINITY;
-            const float lw = lane < NW ? wred[lane * Ws + g * WP + 1] : 0.0f;
+            const float mw = lane < NW ? wred[lane * WS + g * WP] : -INFINITY;
+            const float lw = lane < NW ? wred[lane * WS + g * WP + 1] : 0.0f;
             float mm = mw;
 #pragma unroll
             for (int o2 = 16; o2 > 0; o2 >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o2));
@@ -859,7 +862,7 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
             const int g = i / DP, c = i % DP;
             float s = 0.0f;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * Ws + g * WP + 2 + c], s);
+            for (int w = 0; w < NW; ++w) s = fmaf(shw[w * G + g], wred[w * WS + g * WP + 2 + c], s);
             part[g * (DP + 2) + 2 + c] = s;
         }
         LV9_TRACE(6)

@@ -111,6 +111,27 @@ def main():
               f"last warp -> partial written median {np.median(red):.2f} us")
     # per slot (kv head): the team's survivor cells and when its last CTA finished its tasks
     nb = int(layers[0].geometry().get("team_ctas_per_slot", 18)) if hasattr(layers[0], "geometry") else 18
+    # the CTA of each slot whose wait returned last (dispatched onto a merging SM of the
+    # previous layer): how often it is also the slot's last partial, and how the slot's
+    # partial times follow its survivor counts
+    late_last, late_gap, corr = 0, [], []
+    nslots = 0
+    for l in range(1, L):
+        t = bufs[l].cpu().numpy().astype(np.float64)
+        for sl in range(t.shape[0] // nb):
+            tt = t[sl * nb:(sl + 1) * nb]
+            tt = tt[(tt[:, 13] > 0) & (tt[:, 6] > 0)]
+            if tt.shape[0] < 3:
+                continue
+            nslots += 1
+            il = int(np.argmax(tt[:, 13]))
+            late_last += int(il == int(np.argmax(tt[:, 6])))
+            late_gap.append((tt[il, 6] - np.median(tt[:, 6])) / 1e3)
+            corr.append(np.corrcoef(tt[:, 15], tt[:, 6])[0, 1])
+    if nslots:
+        print(f"late CTA (last wait) is the slot's last partial in {late_last}/{nslots} slots; its partial vs the "
+              f"team median: {np.median(late_gap):+.2f} us; corr(survivor cells, partial time) median "
+              f"{np.nanmedian(corr):.2f}")
     for l in (1, 4):
         t = bufs[l].cpu().numpy().astype(np.float64)
         p0 = t[:, 2][t[:, 2] > 0].min()

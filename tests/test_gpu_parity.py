@@ -416,6 +416,15 @@ def test_layer_query_uneven_teams(torch, oracle, monkeypatch, H_kv, batch, n, sp
     if torch.cuda.get_device_properties(0).multi_processor_count == 148:
         slots = H_kv * batch
         assert layer.geometry()["team_ctas_per_slot"] == -(-148 // slots)
+    # the dense full scan runs the same uneven teams
+    out = torch.zeros((batch, H_kv * 4, 128), dtype=torch.float32, device="cuda")
+    layer.dense_decode(torch.from_numpy(Q).cuda(), out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    for b in range(batch):
+        for hq in range(0, H_kv * 4, 3):
+            w = exact_attention(K[b, hq // 4], V[b, hq // 4], Q[b, hq], np.arange(n))
+            assert rel_err(o[b, hq], w) <= 1e-3, (b, hq)
 
 
 def test_layer_iid_queries_and_extreme_taus(torch, oracle):

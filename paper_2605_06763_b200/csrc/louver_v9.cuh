@@ -820,7 +820,10 @@ __global__ void __launch_bounds__(C9<DP, G>::NTHR, C9<DP, G>::MINB) louver_layer
         static_assert(G * (DP + 4) * 4 <= Ge::PERW, "a warp partial fits its ring area");
         // warp w's partial sits at the start of its own ring area (free once its tasks are
         // done), so a warp writes it as soon as it finishes, with no CTA barrier in front
-        constexpr int WS = Ge::PERW / 4;                            // warp stride in floats
+        // warp stride in floats: the ring area plus 2, so the header reads of lanes w < NW at
+        // w WS (one per warp) fall in distinct banks; the partial stays inside the warp's area
+        constexpr int WS = Ge::PERW / 4 + 2;
+        static_assert(G * (DP + 4) * 4 + 8 * 16 <= Ge::PERW, "the shifted warp partial fits its ring area");
         float* wred = reinterpret_cast<float*>(smem + Ge::OFF_W);  // [NW][WS]
         float* shw = red;                                           // [NW][G] weights
         {

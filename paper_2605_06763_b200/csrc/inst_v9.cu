@@ -37,8 +37,8 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
     int gy = cap / nb;
     if (gy > slots) gy = slots;
     // Every slot resident and SMs left over (148 over 8 slots: 4 idle with teams of 18):
-    // the first cap - nb slots get one CTA more (lists sized for the smaller team, partial
-    // records for vp.nb per slot; vp.nfull != 0 on entry allows it)
+    // the first cap - nb * slots slots get one CTA more (lists sized for the smaller team,
+    // partial records for vp.nb per slot; vp.nfull != 0 on entry allows it)
     int nfull = slots;
     if (vp.nfull && !glist && gy == slots && nb >= 2 && nb + 1 <= vp.nb && cap > nb * slots) {
         nfull = cap - nb * slots < slots ? cap - nb * slots : slots;
@@ -54,6 +54,10 @@ static cudaError_t launch_t(LayerParams vp, int slots, int sms, cudaStream_t st,
         geo[3] = occ;
     }
     cudaLaunchConfig_t cfg{};
+    // spread: grid (slots, team), so the CTAs dispatched last (onto the SMs the previous
+    // layer's merging CTAs free) are one member of each slot. The smaller teams leave
+    // placeholder CTAs at the very end of the order, which exit at once; measured, they are
+    // better than an exact 1-D grid
     if (gy != slots) vp.spread = 0;
     cfg.gridDim = vp.spread ? dim3((unsigned)gy, (unsigned)nb) : dim3((unsigned)nb, (unsigned)gy);
     cfg.blockDim = dim3(Ge::NTHR);
